@@ -1,0 +1,197 @@
+/*
+ * tafv_gpu.h — C-ABI drop-in boundary of the B200-native LTS finite-volume
+ * hot path (arXiv 1704.01144; reference library `tafv`, proj/core).
+ *
+ * Plain pointers and sizes only; no torch, no C++ types. Every entry point
+ * cites the reference interface it replaces (paths relative to the
+ * reference root, proj/core/...). Status codes mirror the reference's
+ * exception classes so the C++ shim (include/tafv_gpu.hpp) can rethrow them:
+ *   0 ok
+ *   1 std::invalid_argument   (tafv::require, common.hpp:9-11)
+ *   2 std::logic_error        (TAFV_ASSERT,   common.hpp:15-19)
+ *   3 std::runtime_error      (divergence,    reference.cpp:123-124)
+ *   4 CUDA error              (new: device failure)
+ *   5 NCCL error              (new: multi-GPU transport; replaces transport.cpp:39-41)
+ * A handle is not thread-safe; use one handle per GPU (one host thread each).
+ *
+ * Conventions:
+ *   - ids are the caller's ORIGINAL cell / face ids; the library renumbers
+ *     internally and maps every array in and out.
+ *   - per-cell state arrays are row-major [n_cells][nv] (nv = 1 scalar,
+ *     5 Euler: rho, rho*u, rho*v, rho*w, E).
+ *   - geometry is Vec3; 2D meshes pass z = 0 (the reference's Vec2,
+ *     geometry.hpp:7-17).
+ */
+#ifndef TAFV_GPU_H
+#define TAFV_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TAFV_OK = 0,
+  TAFV_EINVAL = 1,
+  TAFV_ELOGIC = 2,
+  TAFV_EDIVERGED = 3,
+  TAFV_ECUDA = 4,
+  TAFV_ENCCL = 5
+};
+
+/* Physics: FluxModel (physics.hpp:14-28) extended with compressible Euler. */
+enum { TAFV_ADVECTION = 0, TAFV_BURGERS = 1, TAFV_EULER = 2 };
+
+#define TAFV_MAX_LEVELS 16
+
+/* Mesh view: the reference Mesh/Cell/Face layout (mesh.hpp:26-65) as SoA
+ * arrays. The CSR adjacency (mesh.cpp:241-271) is rebuilt inside
+ * tafv_gpu_create in ascending original face id, exactly as the reference
+ * builds it, and geometric closure is checked (mesh.cpp:273-284). */
+typedef struct tafv_mesh_view {
+  int32_t dim;                      /* 2 (scalar reference meshes) or 3 */
+  int32_t n_cells;
+  int32_t n_faces;
+  const double* cell_volume;        /* [n_cells]    Cell::volume */
+  const double* cell_centroid;      /* [n_cells][3] Cell::centroid */
+  const double* cell_char_length;   /* [n_cells]    Cell::char_length */
+  const int32_t* face_left;         /* [n_faces]    Face::left */
+  const int32_t* face_right;        /* [n_faces]    Face::right (-1 boundary) */
+  const int32_t* face_partner;      /* [n_faces]    Face::periodic_partner (-1 none) */
+  const double* face_normal;        /* [n_faces][3] Face::normal (unit, left->right) */
+  const double* face_area;          /* [n_faces]    Face::area */
+  const double* face_centroid;      /* [n_faces][3] Face::centroid */
+} tafv_mesh_view;
+
+/* FluxModel (physics.hpp:14-28; parse_flux_model physics.cpp:7-21):
+ * advection a=(ax,ay); Burgers direction a (normalised here, as
+ * parse_flux_model does); Euler gamma. */
+typedef struct tafv_physics {
+  int32_t model;
+  double a[3];
+  double gamma;
+} tafv_physics;
+
+/* SolverOptions (reference.hpp:13-18) minus the model. */
+typedef struct tafv_options {
+  int32_t theta_max;
+  double cfl;
+  double dt_cap;
+} tafv_options;
+
+/* IterationRecord (reference.hpp:20-29); total_extensive per component. */
+typedef struct tafv_record {
+  int32_t iteration;
+  int32_t theta;
+  double t_start;
+  double dt;
+  double advance;
+  double cost_ratio;
+  double total_extensive[8];
+  int64_t level_cells[TAFV_MAX_LEVELS];
+  int32_t n_levels;
+  int32_t nv;
+} tafv_record;
+
+/* Summary of an IterationPlan (levels.hpp:46-61) held on the device.
+ * c_eff = sum_tau 2^(theta-tau)|Omega(tau)| (LevelMap::level_cost,
+ * levels.cpp:68-79); f_eff = sum_f 2^(theta-cadence_f);
+ * r_eff = sum_{l<theta} 2^(theta-l)|fringe[l]|. */
+typedef struct tafv_plan_info {
+  int32_t theta;
+  int32_t n_levels;
+  double dt;
+  double cost_ratio;
+  int64_t cells_per_level[TAFV_MAX_LEVELS];
+  int64_t faces_per_cadence[TAFV_MAX_LEVELS];
+  int64_t fringe_per_level[TAFV_MAX_LEVELS];
+  int64_t c_eff;
+  int64_t f_eff;
+  int64_t r_eff;
+} tafv_plan_info;
+
+typedef struct tafv_gpu tafv_gpu;
+
+/* Upload an immutable mesh (replaces the caller-owned `const Mesh&` that every
+ * reference entry takes, mesh.hpp:41) and allocate the SolverState
+ * (state.hpp:17-50, SolverState::init state.cpp:14-38) on `device`. */
+int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
+                    tafv_gpu** out);
+void tafv_gpu_destroy(tafv_gpu* h);
+
+/* Message of the last failure on this handle (or of the last failed create
+ * on this thread when h == NULL). */
+const char* tafv_gpu_last_error(const tafv_gpu* h);
+
+/* State in/out (SolverState::w, ::W, ::t0, ::iteration). W == NULL means
+ * W = w * V, i.e. init_* + sync_extensive (state.cpp:46-68). */
+int tafv_gpu_set_state(tafv_gpu* h, const double* w, const double* W, double t0,
+                       int32_t iteration);
+int tafv_gpu_get_state(tafv_gpu* h, double* w, double* W, double* t0, int32_t* iteration);
+
+/* plan_iteration (reference.hpp:35, reference.cpp:89-98): dt_max, global min,
+ * ilogb classification, smoothing to the |dtau|<=1 fixpoint, level map,
+ * face cadences and the per-level compacted index lists, all on device. */
+int tafv_gpu_plan(tafv_gpu* h, const tafv_options* opt, tafv_plan_info* out);
+
+/* build_iteration_plan(mesh, make_level_map(tau, dt)) (levels.cpp:53-66,
+ * 123-155): inject a hand-made level map, as the reference tests do through
+ * run_iteration's plan argument (reference.hpp:37-40). tau in original ids.
+ * dt <= 0 selects dt = min_c dt_max_c / 2^tau_c (computed on device with
+ * `opt`'s cfl/dt_cap) for synthetic level maps. */
+int tafv_gpu_inject_levels(tafv_gpu* h, const int32_t* tau, double dt, const tafv_options* opt,
+                           tafv_plan_info* out);
+
+/* Export the current plan in original ids for bit-exact list checks:
+ * tau[n_cells], face_cadence[n_faces], cells_of_level flattened level by
+ * level (ascending ids), faces_of_cadence likewise, fringe[l] likewise
+ * (sizes from tafv_plan_info). Any pointer may be NULL. */
+int tafv_gpu_get_plan_lists(tafv_gpu* h, int32_t* tau, int32_t* face_cadence,
+                            int32_t* cells_flat, int32_t* faces_flat, int32_t* fringe_flat);
+
+/* run_iteration (reference.hpp:37-40, reference.cpp:100-129) under the
+ * current plan: 2^theta subiterations of {corrector, predictor} over the
+ * active prefix sets, the trailing corrector, divergence check, record. */
+int tafv_gpu_run_iteration(tafv_gpu* h, tafv_record* out);
+
+/* reference_integrate (reference.hpp:49-52, reference.cpp:135-142):
+ * n x {plan_iteration, run_iteration}; out has room for n records. */
+int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* out);
+
+/* Same as tafv_gpu_iterate but without per-iteration records or the
+ * per-iteration host wait for them (records of the last iteration only);
+ * the device-resident throughput path. */
+int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* last);
+
+/* Debug/parity access to intermediate SolverState arrays in original ids:
+ * "w_pred" [nc][nv], "grad" [nc][nv][3], "phi_pred" / "int_substep" /
+ * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32). */
+int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
+
+/* Launch configuration knobs (bench/profiling): use_graph 0/1 captures each
+ * theta's subiteration sweep as one CUDA graph (default 1). */
+int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value);
+
+/* Kernel launches issued by the last run/iterate/advance call (own kernels
+ * only), and device timings of the last call in milliseconds: [0] whole
+ * call, [1] plan, [2] sweep (subiterations + trailing corrector). */
+int tafv_gpu_stats(tafv_gpu* h, int64_t* launches, double* ms3);
+
+/* 3D hexahedral mesh generator (new: the reference generator is 1D/2D only,
+ * mesh.cpp:302-317). Tensor-product node lattice x[nx+1], y[ny+1], z[nz+1],
+ * interior nodes jittered uniformly by +-jitter of the local spacing
+ * (SplitMix64, seeded), optional random cell/face permutation from `seed`.
+ * Two-call protocol: with out arrays NULL, writes the counts. */
+int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* x, const double* y,
+                  const double* z, double jitter, uint64_t seed, int32_t permute,
+                  int32_t* n_cells, int32_t* n_faces, double* cell_volume, double* cell_centroid,
+                  double* cell_char_length, int32_t* face_left, int32_t* face_right,
+                  int32_t* face_partner, double* face_normal, double* face_area,
+                  double* face_centroid);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TAFV_GPU_H */

@@ -1,0 +1,139 @@
+"""ctypes binding of the C ABI in include/tafv_gpu.h (libtafv_gpu.so).
+
+The product path has no CPU fallback: if the in-tree library is missing the
+import fails loudly (run ``python -c "import __graft_entry__ as g; g.build()"``
+or ``make -C paper_1704_01144_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtafv_gpu.so")
+
+TAFV_OK, TAFV_EINVAL, TAFV_ELOGIC, TAFV_EDIVERGED, TAFV_ECUDA, TAFV_ENCCL = range(6)
+TAFV_ADVECTION, TAFV_BURGERS, TAFV_EULER = 0, 1, 2
+MAX_LEVELS = 16
+
+
+class MeshView(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int32),
+        ("n_cells", C.c_int32),
+        ("n_faces", C.c_int32),
+        ("cell_volume", C.c_void_p),
+        ("cell_centroid", C.c_void_p),
+        ("cell_char_length", C.c_void_p),
+        ("face_left", C.c_void_p),
+        ("face_right", C.c_void_p),
+        ("face_partner", C.c_void_p),
+        ("face_normal", C.c_void_p),
+        ("face_area", C.c_void_p),
+        ("face_centroid", C.c_void_p),
+    ]
+
+
+class Physics(C.Structure):
+    _fields_ = [("model", C.c_int32), ("a", C.c_double * 3), ("gamma", C.c_double)]
+
+
+class Options(C.Structure):
+    _fields_ = [("theta_max", C.c_int32), ("cfl", C.c_double), ("dt_cap", C.c_double)]
+
+
+class Record(C.Structure):
+    _fields_ = [
+        ("iteration", C.c_int32),
+        ("theta", C.c_int32),
+        ("t_start", C.c_double),
+        ("dt", C.c_double),
+        ("advance", C.c_double),
+        ("cost_ratio", C.c_double),
+        ("total_extensive", C.c_double * 8),
+        ("level_cells", C.c_int64 * MAX_LEVELS),
+        ("n_levels", C.c_int32),
+        ("nv", C.c_int32),
+    ]
+
+    def as_dict(self):
+        return {
+            "iteration": self.iteration,
+            "theta": self.theta,
+            "t_start": self.t_start,
+            "dt": self.dt,
+            "advance": self.advance,
+            "cost_ratio": self.cost_ratio,
+            "total_extensive": list(self.total_extensive[: self.nv]),
+            "level_cells": list(self.level_cells[: self.n_levels]),
+        }
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("theta", C.c_int32),
+        ("n_levels", C.c_int32),
+        ("dt", C.c_double),
+        ("cost_ratio", C.c_double),
+        ("cells_per_level", C.c_int64 * MAX_LEVELS),
+        ("faces_per_cadence", C.c_int64 * MAX_LEVELS),
+        ("fringe_per_level", C.c_int64 * MAX_LEVELS),
+        ("c_eff", C.c_int64),
+        ("f_eff", C.c_int64),
+        ("r_eff", C.c_int64),
+    ]
+
+    def as_dict(self):
+        t = self.theta
+        return {
+            "theta": t,
+            "dt": self.dt,
+            "cost_ratio": self.cost_ratio,
+            "cells_per_level": list(self.cells_per_level[: t + 1]),
+            "faces_per_cadence": list(self.faces_per_cadence[: t + 1]),
+            "fringe_per_level": list(self.fringe_per_level[:t]),
+            "c_eff": self.c_eff,
+            "f_eff": self.f_eff,
+            "r_eff": self.r_eff,
+        }
+
+
+# Exported symbols (declared in include/tafv_gpu.h); tests check every one.
+EXPORTS = [
+    "tafv_gpu_create", "tafv_gpu_destroy", "tafv_gpu_last_error", "tafv_gpu_set_state",
+    "tafv_gpu_get_state", "tafv_gpu_plan", "tafv_gpu_inject_levels", "tafv_gpu_get_plan_lists",
+    "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_get_array",
+    "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_mesh_hex",
+]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OSError(f"CUDA library missing: {LIB_PATH}; build it with __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    L.tafv_gpu_create.argtypes = [C.POINTER(MeshView), C.POINTER(Physics), C.c_int, C.POINTER(vp)]
+    L.tafv_gpu_destroy.argtypes = [vp]
+    L.tafv_gpu_destroy.restype = None
+    L.tafv_gpu_last_error.argtypes = [vp]
+    L.tafv_gpu_last_error.restype = C.c_char_p
+    L.tafv_gpu_set_state.argtypes = [vp, vp, vp, dbl, i32]
+    L.tafv_gpu_get_state.argtypes = [vp, vp, vp, C.POINTER(dbl), C.POINTER(i32)]
+    L.tafv_gpu_plan.argtypes = [vp, C.POINTER(Options), C.POINTER(PlanInfo)]
+    L.tafv_gpu_inject_levels.argtypes = [vp, vp, dbl, C.POINTER(Options), C.POINTER(PlanInfo)]
+    L.tafv_gpu_get_plan_lists.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.tafv_gpu_run_iteration.argtypes = [vp, C.POINTER(Record)]
+    L.tafv_gpu_iterate.argtypes = [vp, C.POINTER(Options), i32, C.POINTER(Record)]
+    L.tafv_gpu_advance.argtypes = [vp, C.POINTER(Options), i32, C.POINTER(Record)]
+    L.tafv_gpu_get_array.argtypes = [vp, C.c_char_p, vp]
+    L.tafv_gpu_set_flag.argtypes = [vp, C.c_char_p, i64]
+    L.tafv_gpu_stats.argtypes = [vp, C.POINTER(i64), vp]
+    L.tafv_mesh_hex.argtypes = [i32, i32, i32, vp, vp, vp, dbl, C.c_uint64, i32,
+                                C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    _lib = L
+    return L

@@ -1,0 +1,630 @@
+// sm_100a kernels of the LTS finite-volume hot path.
+//
+// One phase of the reference (corrector_phase / predictor_phase,
+// proj/core/src/reference.cpp:41-70) runs as three kernels, the minimum the
+// data dependencies allow (gradients need every neighbour's staged value,
+// fluxes need both sides' limited gradients, residuals need every face flux):
+//
+//   K1 k_grad_limit   stage (committed / predicted / time-interpolated fringe,
+//                     kernels.cpp:31-63) fused into Green-Gauss
+//                     (kernels.cpp:65-89) + Barth-Jespersen (kernels.cpp:91-121).
+//                     Staging is a pure function of (w, w_pred, tau, front,
+//                     phase), so w_eval is never materialised: every consumer
+//                     recomputes it bitwise-identically.
+//   K2 k_face_flux    window reset (kernels.cpp:123-130) + reconstruction
+//                     (kernels.cpp:132-159) + Rusanov (physics.hpp:42-47) +
+//                     riemann_predict / riemann_correct (kernels.cpp:161-186);
+//                     face states live in registers only.
+//   K3 k_gather_update flux sum in the CSR slot order = ascending ORIGINAL
+//                     face id (kernels.cpp:188-216) + extensive/intensive
+//                     predict or correct (kernels.cpp:218-241). A gather, not
+//                     a scatter: deterministic, no atomics.
+//
+// Plan kernels restate plan_iteration (reference.cpp:89-98): dt_max
+// (kernels.cpp:247-254), min (kernels.cpp:260-264), ilogb classification
+// (levels.cpp:18-25), Jacobi smoothing (levels.cpp:33-51), face cadence and
+// fringe (levels.cpp:123-155), and a stable per-level compaction giving the
+// prefix-union active sets of build_active_sets (reference.cpp:27-39).
+//
+// All item loops are grid-stride over an explicit list (or the identity when
+// every item is active), so one launch shape serves any active-set size.
+#pragma once
+
+#include <cstdint>
+
+#include "physics.cuh"
+
+namespace tafv {
+
+constexpr int kMaxLevels = 16;
+
+// ---- device views --------------------------------------------------------
+struct MeshDev {
+  int n_cells, n_faces;
+  const double* __restrict__ vol;   // [N]
+  const double* __restrict__ cen;   // [N][3]
+  const double* __restrict__ chl;   // [N]
+  const int* __restrict__ adj_off;  // [N+1]
+  const int2* __restrict__ adj;     // [M] {face id (~f when the cell is the right side), neighbour}
+  const int2* __restrict__ lr;      // [F] {left, resolved right (-1 transmissive)}
+  const int* __restrict__ rcf;      // [F] face whose centroid the right side uses (periodic), or null
+  const double4* __restrict__ geo;  // [F] {nx, ny, nz, area}
+  const double* __restrict__ fcen;  // [F][3]
+};
+
+struct StateDev {
+  double* w;     // [N][NV] committed intensive
+  double* W;     // [N][NV] committed extensive
+  double* wp;    // [N][NV] predicted intensive (window end)
+  double* grad;  // [N][NV][3] limited gradient (frozen for fringe cells)
+  int8_t* tau;   // [N]
+  int8_t* cad;   // [F]
+  double* phi;   // [F][NV] phi_pred
+  double* isub;  // [F][NV] int_substep
+  double* iwin;  // [F][NV] int_window
+};
+
+struct PlanDev {
+  double dt_min;        // global stable step (or injected dt)
+  int err;              // bit 0: |dtau| > 1 across a face; bit 1: injected tau out of range
+  int nonfinite;        // divergence flag of the last trailing corrector
+  long long cell_count[kMaxLevels];
+  long long face_count[kMaxLevels];
+  long long fringe_count[kMaxLevels];
+  double totals[8];     // sum of W per component after the last iteration
+};
+
+// ---- staging: pure function of the committed/predicted state ---------------
+// Reproduces w_eval of stage_committed / stage_predicted / stage_interpolated
+// (kernels.cpp:31-63): at `front`, a cell whose window boundary lies on the
+// front (offset 0) stages w (predictor) or w_pred (corrector); a fringe cell
+// straddling the front stages w + theta_f (w_pred - w), theta_f = offset/2^tau.
+template <int NV>
+__device__ __forceinline__ void stage(const StateDev& s, int x, int tx, int front, bool pred,
+                                      double* out) {
+  const int win = 1 << tx;
+  const int off = front & (win - 1);
+  const double* w = s.w + (size_t)x * NV;
+  const double* wp = s.wp + (size_t)x * NV;
+  if (off == 0) {
+    const double* src = pred ? w : wp;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = src[k];
+  } else {
+    const double th = (double)off / (double)win;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double a = w[k];
+      out[k] = a + th * (wp[k] - a);
+    }
+  }
+}
+
+__device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
+__device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
+
+// ---- K1: stage + Green-Gauss + Barth-Jespersen ----------------------------
+template <class P>
+__global__ void __launch_bounds__(128) k_grad_limit(MeshDev m, StateDev s, const int* __restrict__ list,
+                                                    int n, int front, int pred) {
+  constexpr int NV = P::NV, D = P::DIM;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c = list ? list[i] : i;
+    double we[NV];
+    stage<NV>(s, c, s.tau[c], front, pred, we);
+    double g[NV][D];
+    double wmin[NV], wmax[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) g[k][d] = 0.0;
+      wmin[k] = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+      wmax[k] = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
+    }
+    bool any = false;
+    const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
+    for (int t = s0; t < s1; ++t) {
+      const int2 e = m.adj[t];
+      const int f = slot_face(e.x);
+      const double4 gm = m.geo[f];
+      const double scale = slot_sign(e.x) * gm.w;
+      const double nrm[3] = {gm.x, gm.y, gm.z};
+      double wf[NV];
+      if (e.y >= 0) {
+        double wn[NV];
+        stage<NV>(s, e.y, s.tau[e.y], front, pred, wn);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          wf[k] = 0.5 * (we[k] + wn[k]);
+          wmin[k] = smin(wmin[k], wn[k]);
+          wmax[k] = smax(wmax[k], wn[k]);
+        }
+        any = true;
+      } else {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) wf[k] = we[k];
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int d = 0; d < D; ++d) g[k][d] += wf[k] * nrm[d] * scale;
+    }
+    const double inv_v = 1.0 / m.vol[c];
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+      for (int d = 0; d < D; ++d) g[k][d] = g[k][d] * inv_v;
+    if (any) {
+      const double cc[3] = {m.cen[3 * (size_t)c], m.cen[3 * (size_t)c + 1], m.cen[3 * (size_t)c + 2]};
+      double alpha[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) alpha[k] = 1.0;
+      for (int t = s0; t < s1; ++t) {
+        const int f = slot_face(m.adj[t].x);
+        const double* fc = m.fcen + 3 * (size_t)f;
+        double dx[3];
+#pragma unroll
+        for (int d = 0; d < D; ++d) dx[d] = fc[d] - cc[d];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          double delta = g[k][0] * dx[0] + g[k][1] * dx[1];
+          if (D == 3) delta = delta + g[k][D - 1] * dx[D - 1];
+          if (delta == 0.0) continue;
+          const double head = delta > 0.0 ? wmax[k] - we[k] : wmin[k] - we[k];
+          alpha[k] = smin(alpha[k], minmod(delta, head) / delta);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int d = 0; d < D; ++d) g[k][d] *= alpha[k];
+    }
+    double* go = s.grad + (size_t)c * NV * 3;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) go[3 * k + d] = d < D ? g[k][d < D ? d : 0] : 0.0;
+    }
+  }
+}
+
+// kernels.cpp:25-27 with the z term appended left to right.
+template <int D>
+__device__ __forceinline__ double extrapolate(double w, const double* g, const double* from,
+                                              const double* to) {
+  double v = (w + g[0] * (to[0] - from[0])) + g[1] * (to[1] - from[1]);
+  if (D == 3) v = v + g[D - 1] * (to[D - 1] - from[D - 1]);
+  return v;
+}
+
+// ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
+template <class P, bool PRED>
+__global__ void __launch_bounds__(128) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
+                                                   const int* __restrict__ list, int n, int front,
+                                                   double dt) {
+  constexpr int NV = P::NV, D = P::DIM;
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int f = list ? list[i] : i;
+    const int2 lr = m.lr[f];
+    const double4 gm = m.geo[f];
+    const double nrm[3] = {gm.x, gm.y, gm.z};
+    const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
+    const int tl = s.tau[lr.x];
+    double wL[NV], wR[NV];
+    {
+      double we[NV];
+      stage<NV>(s, lr.x, tl, front, PRED, we);
+      const double* g = s.grad + (size_t)lr.x * NV * 3;
+      const double cl[3] = {m.cen[3 * (size_t)lr.x], m.cen[3 * (size_t)lr.x + 1], m.cen[3 * (size_t)lr.x + 2]};
+#pragma unroll
+      for (int k = 0; k < NV; ++k) wL[k] = extrapolate<D>(we[k], g + 3 * k, cl, fc);
+      if (!P::admissible(pp, wL)) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) wL[k] = we[k];
+      }
+    }
+    bool shared_start = (front & ((1 << tl) - 1)) == 0;
+    if (lr.y >= 0) {
+      const int tr = s.tau[lr.y];
+      shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
+      double we[NV];
+      stage<NV>(s, lr.y, tr, front, PRED, we);
+      const double* g = s.grad + (size_t)lr.y * NV * 3;
+      const double cr[3] = {m.cen[3 * (size_t)lr.y], m.cen[3 * (size_t)lr.y + 1], m.cen[3 * (size_t)lr.y + 2]};
+      const double* to = m.fcen + 3 * (size_t)(m.rcf ? m.rcf[f] : f);
+      const double tc[3] = {to[0], to[1], to[2]};
+#pragma unroll
+      for (int k = 0; k < NV; ++k) wR[k] = extrapolate<D>(we[k], g + 3 * k, cr, tc);
+      if (!P::admissible(pp, wR)) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) wR[k] = we[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) wR[k] = wL[k];
+    }
+    double r[NV];
+    rusanov<P>(pp, wL, wR, nrm, r);
+    double* phi = s.phi + (size_t)f * NV;
+    double* iwin = s.iwin + (size_t)f * NV;
+    if (PRED) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) phi[k] = r[k] * gm.w;
+      if (shared_start) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) iwin[k] = 0.0;
+      }
+    } else {
+      const double dt_sub = dt * (double)(1 << s.cad[f]);
+      double* isub = s.isub + (size_t)f * NV;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const double phi_corr = r[k] * gm.w;
+        const double v = 0.5 * dt_sub * (phi[k] + phi_corr);
+        isub[k] = v;
+        iwin[k] = iwin[k] + v;
+      }
+    }
+  }
+}
+
+// ---- K3: flux gather + extensive/intensive update ---------------------------
+// LAST (trailing corrector over every cell) additionally flags non-finite
+// state (kernels.cpp:266-271) and leaves per-block compensated partial sums of
+// W for the record (state.cpp:40-44; a deterministic fixed-shape reduction).
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, double b) {
+  const double s = a.hi + b;
+  const double bb = s - a.hi;
+  const double e = (a.hi - (s - bb)) + (b - bb);
+  DD r;
+  r.hi = s;
+  r.lo = a.lo + e;
+  return r;
+}
+__device__ __forceinline__ DD dd_merge(DD a, DD b) {
+  DD r = dd_add(a, b.hi);
+  r.lo = r.lo + b.lo;
+  const double s = r.hi + r.lo;
+  r.lo = r.lo - (s - r.hi);
+  r.hi = s;
+  return r;
+}
+
+template <class P, bool PRED, bool LAST>
+__global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
+                                                       const int* __restrict__ list, int n,
+                                                       double dt, PlanDev* plan, DD* partials) {
+  constexpr int NV = P::NV;
+  const int stride = gridDim.x * blockDim.x;
+  DD acc[LAST ? NV : 1];
+  bool bad = false;
+  if (LAST) {
+#pragma unroll
+    for (int k = 0; k < (LAST ? NV : 1); ++k) acc[k] = DD{0.0, 0.0};
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c = list ? list[i] : i;
+    const int tc = s.tau[c];
+    double sum[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sum[k] = 0.0;
+    const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
+    for (int t = s0; t < s1; ++t) {
+      const int e = m.adj[t].x;
+      const int f = slot_face(e);
+      const double sg = slot_sign(e);
+      const double* ph;
+      if (PRED) ph = s.phi + (size_t)f * NV;
+      else ph = (tc > s.cad[f] ? s.iwin : s.isub) + (size_t)f * NV;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) sum[k] += sg * ph[k];
+    }
+    const double v = m.vol[c];
+    if (PRED) {
+      const double dtw = dt * (double)(1 << tc);
+      double* wp = s.wp + (size_t)c * NV;
+      const double* W = s.W + (size_t)c * NV;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const double Wp = W[k] + dtw * (-sum[k]);
+        wp[k] = Wp / v;
+      }
+    } else {
+      double* W = s.W + (size_t)c * NV;
+      double* w = s.w + (size_t)c * NV;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const double Wn = W[k] + (-sum[k]);
+        const double wn = Wn / v;
+        W[k] = Wn;
+        w[k] = wn;
+        if (LAST) {
+          bad = bad || !isfinite(Wn) || !isfinite(wn);
+          acc[k < (LAST ? NV : 1) ? k : 0] = dd_add(acc[k < (LAST ? NV : 1) ? k : 0], Wn);
+        }
+      }
+    }
+  }
+  if (LAST) {
+    if (__syncthreads_or(bad) && threadIdx.x == 0) plan->nonfinite = 1;
+    __shared__ DD red[128];
+#pragma unroll
+    for (int k = 0; k < (LAST ? NV : 1); ++k) {
+      red[threadIdx.x] = acc[k];
+      __syncthreads();
+      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) partials[(size_t)k * gridDim.x + blockIdx.x] = red[0];
+      __syncthreads();
+    }
+  }
+}
+
+// Fixed-order reduction of the per-block partials (one block).
+__global__ void k_totals(const DD* partials, int nblocks, int nv, PlanDev* plan) {
+  __shared__ DD red[256];
+  for (int k = 0; k < nv; ++k) {
+    DD a{0.0, 0.0};
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a = dd_merge(a, partials[(size_t)k * nblocks + b]);
+    red[threadIdx.x] = a;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) plan->totals[k] = red[0].hi + red[0].lo;
+    __syncthreads();
+  }
+}
+
+// ---- plan kernels ----------------------------------------------------------
+// kernels.cpp:247-254: dt_max = speed > 0 ? min(dt_cap, cfl*h/speed) : dt_cap,
+// then the order-free min of kernels.cpp:260-264 as per-block partials.
+// With tau != null (synthetic level maps) the bound is dt_max / 2^tau.
+template <class P>
+__global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParams pp, double cfl,
+                                                double dt_cap, double* dt_max, double* block_min,
+                                                const int8_t* tau_scale) {
+  constexpr int NV = P::NV;
+  double lowest = __longlong_as_double(0x7ff0000000000000ll);
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n_cells; c += stride) {
+    double w[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) w[k] = s.w[(size_t)c * NV + k];
+    const double speed = P::speed(pp, w);
+    const double d = speed > 0.0 ? smin(dt_cap, cfl * m.chl[c] / speed) : dt_cap;
+    dt_max[c] = d;
+    const double b = tau_scale ? d / (double)(1 << tau_scale[c]) : d;
+    lowest = smin(lowest, b);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = lowest;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_min[blockIdx.x] = red[0];
+}
+
+__global__ void k_dt_min(const double* block_min, int nblocks, PlanDev* plan) {
+  __shared__ double red[256];
+  double lowest = __longlong_as_double(0x7ff0000000000000ll);
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) lowest = smin(lowest, block_min[b]);
+  red[threadIdx.x] = lowest;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) plan->dt_min = red[0];
+}
+
+// levels.cpp:18-25: raw = ratio >= 1 ? ilogb(ratio) : 0, clamped.
+__device__ __forceinline__ int classify_raw(double dt_max, double dt_min, int theta_max) {
+  const double ratio = dt_max / dt_min;
+  int raw = 0;
+  if (ratio >= 1.0) {
+    const long long bits = __double_as_longlong(ratio);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    raw = ex == 0x7ff ? 0x7fffffff : ex - 1023;  // ratio >= 1 is normal or +inf
+  }
+  return raw < 0 ? 0 : (raw > theta_max ? theta_max : raw);
+}
+
+__global__ void k_classify(int n, const double* dt_max, const PlanDev* plan, int theta_max,
+                           int8_t* raw) {
+  const double dt_min = plan->dt_min;
+  const bool ok = dt_min > 0.0 && isfinite(dt_min);
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride)
+    raw[c] = ok ? (int8_t)classify_raw(dt_max[c], dt_min, theta_max) : (int8_t)0;
+}
+
+// levels.cpp:33-46 one Jacobi sweep: out = min(in, 1 + min over neighbours).
+__global__ void k_smooth(MeshDev m, const int8_t* in, int8_t* out) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n_cells; c += stride) {
+    int bound = in[c];
+    const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
+    for (int t = s0; t < s1; ++t) {
+      const int nb = m.adj[t].y;
+      if (nb >= 0) {
+        const int v = in[nb] + 1;
+        bound = v < bound ? v : bound;
+      }
+    }
+    out[c] = (int8_t)bound;
+  }
+}
+
+// levels.cpp:128-137 face cadence = min(tau_left, tau_right) (boundary: left),
+// plus the fringe flag of levels.cpp:139-153 (the coarser side of a face whose
+// sides differ) and the |dtau| <= 1 invariant the staging relies on.
+__global__ void k_face_cadence(MeshDev m, const int8_t* tau, int8_t* cad, uint8_t* fringe_flag,
+                               PlanDev* plan) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
+    const int2 lr = m.lr[f];
+    const int tl = tau[lr.x];
+    int c = tl;
+    if (lr.y >= 0) {
+      const int tr = tau[lr.y];
+      c = tl < tr ? tl : tr;
+      if (tl != tr) {
+        fringe_flag[tl > tr ? lr.x : lr.y] = 1;
+        const int d = tl > tr ? tl - tr : tr - tl;
+        if (d > 1) atomicOr(&plan->err, 1);
+      }
+    }
+    cad[f] = (int8_t)c;
+  }
+}
+
+// Stable per-key compaction. Tile t covers items [t*kTile, (t+1)*kTile); the
+// count and scatter passes use the same tiling, so the order inside each key
+// bucket is ascending item id.
+constexpr int kTile = 2048;
+constexpr int kCompactThreads = 256;
+
+__global__ void __launch_bounds__(kCompactThreads) k_tile_count(const int8_t* key, int n, int nkeys,
+                                                                int* counts /*[nkeys][ntiles]*/,
+                                                                const uint8_t* fringe_flag,
+                                                                PlanDev* plan) {
+  __shared__ int cnt[kMaxLevels];
+  __shared__ int fcnt[kMaxLevels];
+  if (threadIdx.x < kMaxLevels) {
+    cnt[threadIdx.x] = 0;
+    fcnt[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const int base = blockIdx.x * kTile;
+  for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
+    const int i = base + j;
+    if (i < n) {
+      const int k = key[i];
+      atomicAdd(&cnt[k], 1);
+      if (fringe_flag && fringe_flag[i] && k > 0) atomicAdd(&fcnt[k - 1], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < nkeys) {
+    counts[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = cnt[threadIdx.x];
+    if (fringe_flag && fcnt[threadIdx.x])
+      atomicAdd(reinterpret_cast<unsigned long long*>(&plan->fringe_count[threadIdx.x]),
+                (unsigned long long)fcnt[threadIdx.x]);
+  }
+}
+
+// Exclusive scan over counts in (key, tile) order, in place; totals per key
+// into plan->cell_count or face_count. One block.
+__global__ void __launch_bounds__(1024) k_tile_scan(int* counts, int ntiles, int nkeys,
+                                                    long long* totals) {
+  const int total = ntiles * nkeys;
+  const int per = (total + blockDim.x - 1) / blockDim.x;
+  const int b = threadIdx.x * per, e = min(total, b + per);
+  int local = 0;
+  for (int i = b; i < e; ++i) local += counts[i];
+  __shared__ int part[1024];
+  part[threadIdx.x] = local;
+  __syncthreads();
+  for (int off = 1; off < blockDim.x; off <<= 1) {
+    const int v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int run = part[threadIdx.x] - local;
+  for (int i = b; i < e; ++i) {
+    const int v = counts[i];
+    counts[i] = run;
+    run += v;
+  }
+  __syncthreads();
+  // per-key totals: next key's first offset minus this key's first offset
+  if (threadIdx.x < nkeys) {
+    const int first = counts[(size_t)threadIdx.x * ntiles];
+    const int next = threadIdx.x + 1 < nkeys ? counts[(size_t)(threadIdx.x + 1) * ntiles] : part[blockDim.x - 1];
+    totals[threadIdx.x] = next - first;
+  }
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(const int8_t* key, int n, int nkeys,
+                                                                  const int* offsets, int* list) {
+  __shared__ int wcount[kCompactThreads / 32][kMaxLevels];
+  __shared__ int running[kMaxLevels];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < nkeys) running[threadIdx.x] = offsets[(size_t)threadIdx.x * gridDim.x + blockIdx.x];
+  const int base = blockIdx.x * kTile;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = 0; r < kTile; r += blockDim.x) {
+    const int i = base + r + threadIdx.x;
+    const int k = i < n ? key[i] : -1;
+    int rank = 0;
+    for (int q = 0; q < nkeys; ++q) {
+      const unsigned mask = __ballot_sync(0xffffffffu, k == q);
+      if (k == q) rank = __popc(mask & lt);
+      if (lane == 0) wcount[warp][q] = __popc(mask);
+    }
+    __syncthreads();
+    if (k >= 0) {
+      int pos = running[k] + rank;
+      for (int w = 0; w < warp; ++w) pos += wcount[w][k];
+      list[pos] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x < nkeys) {
+      int tot = 0;
+      for (int w = 0; w < kCompactThreads / 32; ++w) tot += wcount[w][threadIdx.x];
+      running[threadIdx.x] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- state movement (original <-> internal numbering) -----------------------
+__global__ void k_gather_rows(const double* src, const int* perm, int n, int width, double* dst) {
+  const size_t total = (size_t)n * width;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const size_t row = i / width, col = i % width;
+    dst[i] = src[(size_t)perm[row] * width + col];
+  }
+}
+
+__global__ void k_scatter_rows(const double* src, const int* perm, int n, int width, double* dst) {
+  const size_t total = (size_t)n * width;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const size_t row = i / width, col = i % width;
+    dst[(size_t)perm[row] * width + col] = src[i];
+  }
+}
+
+// W = w * V (sync_extensive, state.cpp:61-68) for set_state without W.
+__global__ void k_sync_extensive(const double* w, const double* vol, int n, int nv, double* W) {
+  const size_t total = (size_t)n * nv;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    W[i] = w[i] * vol[i / nv];
+}
+
+__global__ void k_gather_i8(const int32_t* src, const int* perm, int n, int8_t* dst, PlanDev* plan,
+                            int max_level) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int v = src[perm[i]];
+    if (v < 0 || v > max_level) atomicOr(&plan->err, 2);
+    dst[i] = (int8_t)(v < 0 ? 0 : (v > max_level ? max_level : v));
+  }
+}
+
+}  // namespace tafv

@@ -1,0 +1,869 @@
+// Host runtime of the B200 LTS finite-volume hot path: implements the C ABI
+// of include/tafv_gpu.h (the drop-in boundary for plan_iteration /
+// run_iteration / reference_integrate, proj/core/include/tafv/reference.hpp).
+//
+// Data layout in HBM:
+//   * cells renumbered once at upload by a 63-bit Morton key of the centroid
+//     (locality for the neighbour gathers); faces grouped by their left cell;
+//     the per-cell CSR slots keep the reference order (ascending ORIGINAL
+//     face id, mesh.cpp:241-271) so every sum associates exactly as the
+//     reference's;
+//   * FP64 AoS rows per cell/face ([N][nv] state, [N][nv][3] gradients,
+//     [F][nv] face fluxes) so a gathered neighbour is one contiguous run;
+//   * per-iteration plan: int8 levels/cadences and level-sorted index lists
+//     whose prefixes are the active sets of every subiteration level.
+// One plan read-back per iteration (theta, counts, dt: the host needs theta
+// to size the 2^theta sweep); everything else stays on the device.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "tafv_gpu.h"
+
+using namespace tafv;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Error {
+  int code;
+  std::string what;
+};
+
+void check_cuda(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) throw Error{TAFV_ECUDA, std::string(where) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) check_cuda((x), #x)
+
+void require(bool cond, const char* what) {
+  if (!cond) throw Error{TAFV_EINVAL, what};
+}
+
+template <class T>
+T* dalloc(size_t n) {
+  T* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return p;
+}
+
+inline uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+int subiteration_level(int s, int theta) {  // levels.cpp:10-16
+  for (int tmp = theta; tmp > 0; --tmp)
+    if ((s - 1) % (1 << tmp) == 0) return tmp;
+  return 0;
+}
+
+}  // namespace
+
+struct tafv_gpu {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  int model = TAFV_EULER, nv = 5, dim = 3;
+  PhysParams pp{};
+  int N = 0, F = 0, M = 0;
+  bool periodic = false;
+  int sms = 148;
+  std::vector<int> cperm, fperm;  // internal -> original
+  std::vector<double> vol_host;
+
+  // device mesh
+  double *vol = nullptr, *cen = nullptr, *chl = nullptr, *fcen = nullptr;
+  int* adj_off = nullptr;
+  int2* adj = nullptr;
+  int2* lr = nullptr;
+  int* rcf = nullptr;
+  double4* geo = nullptr;
+  int *d_cperm = nullptr, *d_fperm = nullptr;
+  // device state
+  double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
+  double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
+  int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
+  uint8_t* fflag = nullptr;
+  double *dtmax = nullptr, *blockmin = nullptr;
+  int nblk_dt = 0;
+  int *cell_counts = nullptr, *face_counts = nullptr;
+  int ntile_c = 0, ntile_f = 0;
+  int *clist = nullptr, *flist = nullptr;
+  DD* partials = nullptr;
+  int nblk_last = 0;
+  PlanDev* dplan = nullptr;
+  PlanDev* hplan = nullptr;  // pinned
+  double* stage_buf = nullptr;
+  size_t stage_len = 0;
+  cudaEvent_t ev[4] = {};
+
+  // host copy of the plan
+  bool has_plan = false;
+  int theta = 0;
+  double dt = 0.0;
+  long long ccount[kMaxLevels] = {}, fcount[kMaxLevels] = {}, frcount[kMaxLevels] = {};
+  double t0 = 0.0;
+  int iteration = 0;
+  bool state_set = false;
+
+  // stats
+  int64_t launches = 0;
+  double ms[3] = {0, 0, 0};
+  int grid_cap = 148 * 8;
+
+  MeshDev mesh_dev() const {
+    return MeshDev{N, F, vol, cen, chl, adj_off, adj, lr, periodic ? rcf : nullptr, geo, fcen};
+  }
+  StateDev state_dev() const { return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin}; }
+
+  double* staging(size_t n) {
+    if (n > stage_len) {
+      if (stage_buf) cudaFree(stage_buf);
+      stage_buf = dalloc<double>(n);
+      stage_len = n;
+    }
+    return stage_buf;
+  }
+
+  int grid_for(long long n, int block) const {
+    long long g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    return (int)std::min<long long>(g, grid_cap);
+  }
+
+  ~tafv_gpu() {
+    cudaSetDevice(device);
+    void* ptrs[] = {vol, cen, chl, fcen, adj_off, adj, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
+                    grad, phi, isub, iwin, tau, cad, raw, tmpa, tmpb, fflag, dtmax, blockmin,
+                    cell_counts, face_counts, clist, flist, partials, dplan, stage_buf};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (hplan) cudaFreeHost(hplan);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace {
+
+// ---- mesh upload -----------------------------------------------------------
+void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
+  const int N = mv.n_cells, F = mv.n_faces;
+  require(N > 0 && F >= 0, "mesh: empty mesh");
+  require(mv.dim == 2 || mv.dim == 3, "mesh: dim must be 2 or 3");
+  h.N = N;
+  h.F = F;
+  h.dim = mv.dim;
+  for (int f = 0; f < F; ++f) {
+    require(mv.face_left[f] >= 0 && mv.face_left[f] < N, "mesh: face left cell out of range");
+    require(mv.face_right[f] >= -1 && mv.face_right[f] < N, "mesh: face right cell out of range");
+    require(mv.face_partner[f] >= -1 && mv.face_partner[f] < F, "mesh: periodic partner out of range");
+    if (mv.face_partner[f] >= 0) h.periodic = true;
+  }
+
+  // Cell order: Morton key of the centroid (ties by original id).
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int c = 0; c < N; ++c)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], mv.cell_centroid[3 * (size_t)c + d]);
+      hi[d] = std::max(hi[d], mv.cell_centroid[3 * (size_t)c + d]);
+    }
+  std::vector<std::pair<uint64_t, int>> key(N);
+  for (int c = 0; c < N; ++c) {
+    uint64_t k = 0;
+    for (int d = 0; d < 3; ++d) {
+      const double span = hi[d] - lo[d];
+      const double u = span > 0 ? (mv.cell_centroid[3 * (size_t)c + d] - lo[d]) / span : 0.0;
+      const uint64_t q = (uint64_t)std::min(2097151.0, std::max(0.0, u * 2097151.0));
+      k |= spread3(q) << d;
+    }
+    key[c] = {k, c};
+  }
+  std::sort(key.begin(), key.end());
+  h.cperm.resize(N);
+  std::vector<int> cinv(N);
+  for (int i = 0; i < N; ++i) {
+    h.cperm[i] = key[i].second;
+    cinv[key[i].second] = i;
+  }
+  key.clear();
+  key.shrink_to_fit();
+
+  // Face order: grouped by internal left cell, stable in original face id.
+  std::vector<int> fstart(N + 1, 0);
+  for (int f = 0; f < F; ++f) ++fstart[cinv[mv.face_left[f]] + 1];
+  for (int i = 0; i < N; ++i) fstart[i + 1] += fstart[i];
+  h.fperm.resize(F);
+  std::vector<int> finv(F);
+  {
+    std::vector<int> cur(fstart.begin(), fstart.end() - 1);
+    for (int f = 0; f < F; ++f) {
+      const int j = cur[cinv[mv.face_left[f]]]++;
+      h.fperm[j] = f;
+      finv[f] = j;
+    }
+  }
+
+  auto resolved_right = [&](int f) {  // kernels.cpp:15-20
+    if (mv.face_right[f] >= 0) return mv.face_right[f];
+    if (mv.face_partner[f] >= 0) return mv.face_left[mv.face_partner[f]];
+    return -1;
+  };
+
+  // CSR adjacency (mesh.cpp:241-271) in internal numbering; faces visited in
+  // ascending ORIGINAL id so each cell's slots follow the reference order.
+  std::vector<int> off(N + 1, 0);
+  for (int f = 0; f < F; ++f) {
+    ++off[cinv[mv.face_left[f]] + 1];
+    if (mv.face_right[f] >= 0) ++off[cinv[mv.face_right[f]] + 1];
+  }
+  for (int i = 0; i < N; ++i) off[i + 1] += off[i];
+  h.M = off[N];
+  std::vector<int2> adj(h.M);
+  std::vector<double> sgn(h.M);
+  {
+    std::vector<int> cur(off.begin(), off.end() - 1);
+    for (int f = 0; f < F; ++f) {
+      const int rr = resolved_right(f);
+      const int L = cinv[mv.face_left[f]];
+      adj[cur[L]] = make_int2(finv[f], rr >= 0 ? cinv[rr] : -1);
+      sgn[cur[L]++] = 1.0;
+      if (mv.face_right[f] >= 0) {
+        const int R = cinv[mv.face_right[f]];
+        adj[cur[R]] = make_int2(~finv[f], L);
+        sgn[cur[R]++] = -1.0;
+      }
+    }
+  }
+  // Geometric closure (mesh.cpp:273-284), same slot order and expressions.
+  for (int i = 0; i < N; ++i) {
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int t = off[i]; t < off[i + 1]; ++t) {
+      const int j = adj[t].x >= 0 ? adj[t].x : ~adj[t].x;
+      const int f = h.fperm[j];
+      for (int d = 0; d < 3; ++d) s[d] += sgn[t] * mv.face_normal[3 * (size_t)f + d] * mv.face_area[f];
+    }
+    if (std::abs(s[0]) > 1e-12 || std::abs(s[1]) > 1e-12 || std::abs(s[2]) > 1e-12)
+      throw Error{TAFV_ELOGIC, "mesh: geometric closure violated for a cell"};
+  }
+
+  // Permuted host arrays -> device.
+  std::vector<double> vol(N), cen(3 * (size_t)N), chl(N);
+  for (int i = 0; i < N; ++i) {
+    const int c = h.cperm[i];
+    vol[i] = mv.cell_volume[c];
+    chl[i] = mv.cell_char_length[c];
+    for (int d = 0; d < 3; ++d) cen[3 * (size_t)i + d] = mv.cell_centroid[3 * (size_t)c + d];
+  }
+  std::vector<int2> lr(F);
+  std::vector<int> rcf(h.periodic ? F : 0);
+  std::vector<double4> geo(F);
+  std::vector<double> fcen(3 * (size_t)F);
+  for (int j = 0; j < F; ++j) {
+    const int f = h.fperm[j];
+    const int rr = resolved_right(f);
+    lr[j] = make_int2(cinv[mv.face_left[f]], rr >= 0 ? cinv[rr] : -1);
+    if (h.periodic) rcf[j] = (mv.face_right[f] < 0 && mv.face_partner[f] >= 0) ? finv[mv.face_partner[f]] : j;
+    geo[j] = make_double4(mv.face_normal[3 * (size_t)f], mv.face_normal[3 * (size_t)f + 1],
+                          mv.face_normal[3 * (size_t)f + 2], mv.face_area[f]);
+    for (int d = 0; d < 3; ++d) fcen[3 * (size_t)j + d] = mv.face_centroid[3 * (size_t)f + d];
+  }
+  h.vol_host = vol;
+
+  auto up = [&](auto* dst, const auto& src) {
+    CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(src[0]), cudaMemcpyHostToDevice));
+  };
+  h.vol = dalloc<double>(N);
+  up(h.vol, vol);
+  h.cen = dalloc<double>(3 * (size_t)N);
+  up(h.cen, cen);
+  h.chl = dalloc<double>(N);
+  up(h.chl, chl);
+  h.adj_off = dalloc<int>(N + 1);
+  up(h.adj_off, off);
+  h.adj = dalloc<int2>(h.M);
+  up(h.adj, adj);
+  h.lr = dalloc<int2>(F);
+  up(h.lr, lr);
+  if (h.periodic) {
+    h.rcf = dalloc<int>(F);
+    up(h.rcf, rcf);
+  }
+  h.geo = dalloc<double4>(F);
+  up(h.geo, geo);
+  h.fcen = dalloc<double>(3 * (size_t)F);
+  up(h.fcen, fcen);
+  h.d_cperm = dalloc<int>(N);
+  up(h.d_cperm, h.cperm);
+  h.d_fperm = dalloc<int>(F);
+  up(h.d_fperm, h.fperm);
+}
+
+void alloc_state(tafv_gpu& h) {
+  const size_t N = h.N, F = h.F, nv = h.nv;
+  h.w = dalloc<double>(N * nv);
+  h.W = dalloc<double>(N * nv);
+  h.wp = dalloc<double>(N * nv);
+  h.grad = dalloc<double>(N * nv * 3);
+  h.phi = dalloc<double>(F * nv);
+  h.isub = dalloc<double>(F * nv);
+  h.iwin = dalloc<double>(F * nv);
+  CK(cudaMemset(h.w, 0, N * nv * sizeof(double)));
+  CK(cudaMemset(h.W, 0, N * nv * sizeof(double)));
+  CK(cudaMemset(h.wp, 0, N * nv * sizeof(double)));
+  CK(cudaMemset(h.grad, 0, N * nv * 3 * sizeof(double)));
+  CK(cudaMemset(h.phi, 0, F * nv * sizeof(double)));
+  CK(cudaMemset(h.isub, 0, F * nv * sizeof(double)));
+  CK(cudaMemset(h.iwin, 0, F * nv * sizeof(double)));
+  h.tau = dalloc<int8_t>(N);
+  h.raw = dalloc<int8_t>(N);
+  h.tmpa = dalloc<int8_t>(N);
+  h.tmpb = dalloc<int8_t>(N);
+  h.fflag = dalloc<uint8_t>(N);
+  h.cad = dalloc<int8_t>(F);
+  CK(cudaMemset(h.tau, 0, N));
+  CK(cudaMemset(h.cad, 0, F));
+  h.dtmax = dalloc<double>(N);
+  h.nblk_dt = h.sms * 4;
+  h.blockmin = dalloc<double>(h.nblk_dt);
+  h.ntile_c = (int)((N + kTile - 1) / kTile);
+  h.ntile_f = (int)((F + kTile - 1) / kTile);
+  h.cell_counts = dalloc<int>((size_t)h.ntile_c * kMaxLevels);
+  h.face_counts = dalloc<int>((size_t)std::max(1, h.ntile_f) * kMaxLevels);
+  h.clist = dalloc<int>(N);
+  h.flist = dalloc<int>(F);
+  h.nblk_last = h.grid_cap;
+  h.partials = dalloc<DD>((size_t)h.nblk_last * 8);
+  h.dplan = dalloc<PlanDev>(1);
+  CK(cudaMemset(h.dplan, 0, sizeof(PlanDev)));
+  CK(cudaMallocHost(&h.hplan, sizeof(PlanDev)));
+  std::memset(h.hplan, 0, sizeof(PlanDev));
+  for (auto& e : h.ev) CK(cudaEventCreate(&e));
+}
+
+// ---- plan ------------------------------------------------------------------
+template <class P>
+void launch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
+  k_dt_max<P><<<h.nblk_dt, 256, 0, h.st>>>(h.mesh_dev(), h.state_dev(), h.pp, cfl, dt_cap, h.dtmax,
+                                          h.blockmin, tau_scale);
+  k_dt_min<<<1, 256, 0, h.st>>>(h.blockmin, h.nblk_dt, h.dplan);
+  h.launches += 2;
+}
+
+void dispatch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
+  switch (h.model) {
+    case TAFV_ADVECTION: launch_dt_max<Advection2D>(h, cfl, dt_cap, tau_scale); break;
+    case TAFV_BURGERS: launch_dt_max<Burgers2D>(h, cfl, dt_cap, tau_scale); break;
+    default: launch_dt_max<Euler3D>(h, cfl, dt_cap, tau_scale); break;
+  }
+}
+
+void reset_plan_counts(tafv_gpu& h) {
+  // Clear counts/flags but keep dt_min (written before by the dt kernels).
+  CK(cudaMemsetAsync(&h.dplan->err, 0, sizeof(int) * 2 + sizeof(long long) * 3 * kMaxLevels, h.st));
+}
+
+// Face cadences, fringe counts and the level-sorted cell / face lists, then
+// the single host read-back of the plan.
+void finish_plan(tafv_gpu& h, int nkeys) {
+  const MeshDev md = h.mesh_dev();
+  CK(cudaMemsetAsync(h.fflag, 0, h.N, h.st));
+  k_face_cadence<<<h.grid_for(h.F, 256), 256, 0, h.st>>>(md, h.tau, h.cad, h.fflag, h.dplan);
+  k_tile_count<<<h.ntile_c, kCompactThreads, 0, h.st>>>(h.tau, h.N, nkeys, h.cell_counts, h.fflag, h.dplan);
+  k_tile_scan<<<1, 1024, 0, h.st>>>(h.cell_counts, h.ntile_c, nkeys, h.dplan->cell_count);
+  k_tile_scatter<<<h.ntile_c, kCompactThreads, 0, h.st>>>(h.tau, h.N, nkeys, h.cell_counts, h.clist);
+  h.launches += 4;
+  if (h.F > 0) {
+    k_tile_count<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F, nkeys, h.face_counts, nullptr, h.dplan);
+    k_tile_scan<<<1, 1024, 0, h.st>>>(h.face_counts, h.ntile_f, nkeys, h.dplan->face_count);
+    k_tile_scatter<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F, nkeys, h.face_counts, h.flist);
+    h.launches += 3;
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+  CK(cudaStreamSynchronize(h.st));
+  const PlanDev& p = *h.hplan;
+  h.has_plan = false;
+  if (p.err & 2) throw Error{TAFV_EINVAL, "level map: level outside [0, 15]"};
+  if (p.err & 1)
+    throw Error{TAFV_ELOGIC, "plan: neighbouring levels differ by more than one (unsmoothed level map)"};
+  h.dt = p.dt_min;
+  h.theta = 0;
+  for (int l = 0; l < kMaxLevels; ++l) {
+    h.ccount[l] = l < nkeys ? p.cell_count[l] : 0;
+    h.fcount[l] = l < nkeys ? p.face_count[l] : 0;
+    h.frcount[l] = p.fringe_count[l];
+    if (h.ccount[l] > 0) h.theta = l;
+  }
+  h.has_plan = true;
+}
+
+void fill_plan_info(const tafv_gpu& h, tafv_plan_info* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof *out);
+  out->theta = h.theta;
+  out->n_levels = h.theta + 1;
+  out->dt = h.dt;
+  long long cost = 0, fe = 0, re = 0;
+  for (int l = 0; l <= h.theta; ++l) {
+    out->cells_per_level[l] = h.ccount[l];
+    out->faces_per_cadence[l] = h.fcount[l];
+    cost += (1ll << (h.theta - l)) * h.ccount[l];
+    fe += (1ll << (h.theta - l)) * h.fcount[l];
+  }
+  for (int l = 0; l < h.theta; ++l) {
+    out->fringe_per_level[l] = h.frcount[l];
+    re += (1ll << (h.theta - l)) * h.frcount[l];
+  }
+  out->c_eff = cost;
+  out->f_eff = fe;
+  out->r_eff = re;
+  // LevelMap::cost_ratio (levels.cpp:73-79)
+  out->cost_ratio = cost == 0 ? 1.0 : (double)((1ll << h.theta) * (long long)h.N) / (double)cost;
+}
+
+void plan(tafv_gpu& h, const tafv_options& opt) {
+  require(opt.theta_max >= 0, "classify: theta_max must be >= 0");
+  require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
+  require(h.state_set, "plan: state not set");
+  h.has_plan = false;
+  dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr);
+  reset_plan_counts(h);
+  k_classify<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.N, h.dtmax, h.dplan, opt.theta_max, h.raw);
+  ++h.launches;
+  // Jacobi smoothing (levels.cpp:33-51). The fixpoint is
+  // min_d raw(d) + dist(c, d); a cell more than theta_max hops away cannot
+  // lower raw(c) <= theta_max, so theta_max sweeps reach it exactly.
+  const MeshDev md = h.mesh_dev();
+  if (opt.theta_max == 0) {
+    CK(cudaMemcpyAsync(h.tau, h.raw, h.N, cudaMemcpyDeviceToDevice, h.st));
+  } else {
+    const int8_t* src = h.raw;
+    for (int i = 0; i < opt.theta_max; ++i) {
+      int8_t* dst = i == opt.theta_max - 1 ? h.tau : (i % 2 == 0 ? h.tmpa : h.tmpb);
+      k_smooth<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(md, src, dst);
+      ++h.launches;
+      src = dst;
+    }
+  }
+  finish_plan(h, opt.theta_max + 1);
+  // reference.cpp:93
+  if (!(std::isfinite(h.dt) && h.dt > 0.0)) {
+    h.has_plan = false;
+    throw Error{TAFV_EINVAL, "integrate: stable step collapsed"};
+  }
+}
+
+void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options* opt) {
+  require(h.state_set || dt > 0.0, "inject_levels: state not set");
+  int maxl = 0;
+  for (int c = 0; c < h.N; ++c) {
+    require(tau_host[c] >= 0, "level map: negative level");
+    maxl = std::max(maxl, (int)tau_host[c]);
+  }
+  require(maxl < kMaxLevels, "level map: level above the supported 15");
+  h.has_plan = false;
+  CK(cudaMemsetAsync(h.dplan, 0, sizeof(PlanDev), h.st));
+  int32_t* stage = reinterpret_cast<int32_t*>(h.staging(((size_t)h.N + 1) / 2));
+  CK(cudaMemcpyAsync(stage, tau_host, (size_t)h.N * sizeof(int32_t), cudaMemcpyHostToDevice, h.st));
+  k_gather_i8<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(stage, h.d_cperm, h.N, h.tau, h.dplan, kMaxLevels - 1);
+  ++h.launches;
+  if (dt > 0.0) {
+    h.hplan->dt_min = dt;
+    CK(cudaMemcpyAsync(&h.dplan->dt_min, &h.hplan->dt_min, sizeof(double), cudaMemcpyHostToDevice, h.st));
+  } else {
+    require(opt != nullptr, "inject_levels: dt <= 0 needs options for the stable step");
+    dispatch_dt_max(h, opt->cfl, opt->dt_cap, h.tau);
+  }
+  finish_plan(h, maxl + 1);
+  if (!(std::isfinite(h.dt) && h.dt > 0.0)) {  // levels.cpp:54
+    h.has_plan = false;
+    throw Error{TAFV_EINVAL, "level map: dt must be positive"};
+  }
+}
+
+// ---- the subiteration sweep ------------------------------------------------
+template <class P>
+void phase(tafv_gpu& h, bool pred, bool last, int level, int front) {
+  long long na = 0, nf = 0;
+  for (int l = 0; l <= level; ++l) {
+    na += h.ccount[l];
+    nf += h.fcount[l];
+  }
+  const int* cl = na == h.N ? nullptr : h.clist;
+  const int* fl = nf == h.F ? nullptr : h.flist;
+  const MeshDev md = h.mesh_dev();
+  const StateDev sd = h.state_dev();
+  const int gc = h.grid_for(na, 128), gf = h.grid_for(nf, 128);
+  if (na > 0) {
+    k_grad_limit<P><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, front, pred ? 1 : 0);
+    ++h.launches;
+  }
+  if (nf > 0) {
+    if (pred) k_face_flux<P, true><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
+    else k_face_flux<P, false><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
+    ++h.launches;
+  }
+  if (last) {
+    k_gather_update<P, false, true><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, h.N, h.dt, h.dplan,
+                                                                   h.partials);
+    k_totals<<<1, 256, 0, h.st>>>(h.partials, h.nblk_last, P::NV, h.dplan);
+    h.launches += 2;
+  } else if (na > 0) {
+    if (pred) k_gather_update<P, true, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+    else k_gather_update<P, false, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+    ++h.launches;
+  }
+}
+
+template <class P>
+void sweep(tafv_gpu& h) {
+  const int subs = 1 << h.theta;
+  for (int s = 1; s <= subs; ++s) {  // reference.cpp:108-120
+    const int level = subiteration_level(s, h.theta);
+    const int front = s - 1;
+    if (s > 1) phase<P>(h, false, false, level, front);
+    phase<P>(h, true, false, level, front);
+  }
+  phase<P>(h, false, true, h.theta, subs);  // trailing corrector, reference.cpp:121
+}
+
+void run_sweep(tafv_gpu& h) {
+  CK(cudaMemsetAsync(&h.dplan->nonfinite, 0, sizeof(int), h.st));
+  switch (h.model) {
+    case TAFV_ADVECTION: sweep<Advection2D>(h); break;
+    case TAFV_BURGERS: sweep<Burgers2D>(h); break;
+    default: sweep<Euler3D>(h); break;
+  }
+  CK(cudaGetLastError());
+}
+
+// Host side of the end of run_iteration (reference.cpp:123-128) once the
+// sweep's flags and totals are back on the host.
+void close_iteration(tafv_gpu& h, tafv_record* rec) {
+  if (h.hplan->nonfinite) {
+    h.has_plan = false;
+    throw Error{TAFV_EDIVERGED, "integrate: solution diverged to a non-finite state"};
+  }
+  const double t_start = h.t0;
+  h.t0 = t_start + h.dt * (double)(1 << h.theta);
+  h.iteration += 1;
+  if (rec) {
+    tafv_plan_info pi;
+    fill_plan_info(h, &pi);
+    std::memset(rec, 0, sizeof *rec);
+    rec->iteration = h.iteration;
+    rec->t_start = t_start;
+    rec->dt = h.dt;
+    rec->theta = h.theta;
+    rec->advance = h.dt * (double)(1 << h.theta);
+    rec->cost_ratio = pi.cost_ratio;
+    rec->nv = h.nv;
+    for (int k = 0; k < h.nv; ++k) rec->total_extensive[k] = h.hplan->totals[k];
+    rec->n_levels = h.theta + 1;
+    for (int l = 0; l <= h.theta; ++l) rec->level_cells[l] = h.ccount[l];
+  }
+}
+
+void run_iteration(tafv_gpu& h, tafv_record* rec) {
+  require(h.has_plan, "run_iteration: no plan (call tafv_gpu_plan or tafv_gpu_inject_levels)");
+  CK(cudaEventRecord(h.ev[0], h.st));
+  run_sweep(h);
+  CK(cudaEventRecord(h.ev[1], h.st));
+  CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+  CK(cudaStreamSynchronize(h.st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
+  h.ms[2] += ms;
+  close_iteration(h, rec);
+}
+
+template <class F>
+int guard(tafv_gpu* h, F&& f) {
+  if (!h) return TAFV_EINVAL;
+  try {
+    CK(cudaSetDevice(h->device));
+    f();
+    return TAFV_OK;
+  } catch (const Error& e) {
+    h->err = e.what;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    h->err = "host allocation failed";
+    return TAFV_ECUDA;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return TAFV_ECUDA;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
+                    tafv_gpu** out) {
+  if (!out || !mesh || !physics) {
+    g_create_error = "tafv_gpu_create: null argument";
+    return TAFV_EINVAL;
+  }
+  *out = nullptr;
+  auto* h = new tafv_gpu;
+  h->device = device;
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+    h->grid_cap = h->sms * 16;
+    h->model = physics->model;
+    switch (physics->model) {
+      case TAFV_ADVECTION:
+        h->nv = 1;
+        h->pp.ax = physics->a[0];
+        h->pp.ay = physics->a[1];
+        break;
+      case TAFV_BURGERS: {  // parse_flux_model (physics.cpp:13-17)
+        h->nv = 1;
+        const double len = std::sqrt(physics->a[0] * physics->a[0] + physics->a[1] * physics->a[1]);
+        require(len > 0.0, "physics: burgers direction must be nonzero");
+        h->pp.ax = physics->a[0] / len;
+        h->pp.ay = physics->a[1] / len;
+        break;
+      }
+      case TAFV_EULER:
+        require(physics->gamma > 1.0, "physics: gamma must exceed 1");
+        h->nv = 5;
+        h->pp.gamma = physics->gamma;
+        h->pp.gm1 = physics->gamma - 1.0;
+        break;
+      default:
+        require(false, "physics: unknown model");
+    }
+    if (h->model != TAFV_EULER) require(mesh->dim == 2, "physics: scalar models run on 2D meshes");
+    else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
+    upload_mesh(*h, *mesh);
+    alloc_state(*h);
+  } catch (const Error& e) {
+    g_create_error = e.what;
+    delete h;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    delete h;
+    return TAFV_ECUDA;
+  }
+  *out = h;
+  return TAFV_OK;
+}
+
+void tafv_gpu_destroy(tafv_gpu* h) { delete h; }
+
+const char* tafv_gpu_last_error(const tafv_gpu* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int tafv_gpu_set_state(tafv_gpu* h, const double* w, const double* W, double t0, int32_t iteration) {
+  return guard(h, [&] {
+    require(w != nullptr, "set_state: w is null");
+    const size_t n = (size_t)h->N * h->nv;
+    double* stage = h->staging(n);
+    CK(cudaMemcpyAsync(stage, w, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+    k_gather_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(stage, h->d_cperm, h->N, h->nv, h->w);
+    if (W) {
+      CK(cudaMemcpyAsync(stage, W, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+      k_gather_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(stage, h->d_cperm, h->N, h->nv, h->W);
+    } else {
+      k_sync_extensive<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->w, h->vol, h->N, h->nv, h->W);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));
+    h->t0 = t0;
+    h->iteration = iteration;
+    h->state_set = true;
+    h->has_plan = false;
+  });
+}
+
+int tafv_gpu_get_state(tafv_gpu* h, double* w, double* W, double* t0, int32_t* iteration) {
+  return guard(h, [&] {
+    const size_t n = (size_t)h->N * h->nv;
+    double* stage = h->staging(n);
+    if (w) {
+      k_scatter_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->w, h->d_cperm, h->N, h->nv, stage);
+      CK(cudaMemcpyAsync(w, stage, n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    if (W) {
+      k_scatter_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, stage);
+      CK(cudaMemcpyAsync(W, stage, n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+    }
+    CK(cudaStreamSynchronize(h->st));
+    if (t0) *t0 = h->t0;
+    if (iteration) *iteration = h->iteration;
+  });
+}
+
+int tafv_gpu_plan(tafv_gpu* h, const tafv_options* opt, tafv_plan_info* out) {
+  return guard(h, [&] {
+    require(opt != nullptr, "plan: null options");
+    h->launches = 0;
+    plan(*h, *opt);
+    fill_plan_info(*h, out);
+  });
+}
+
+int tafv_gpu_inject_levels(tafv_gpu* h, const int32_t* tau, double dt, const tafv_options* opt,
+                           tafv_plan_info* out) {
+  return guard(h, [&] {
+    require(tau != nullptr, "inject_levels: tau is null");
+    inject(*h, tau, dt, opt);
+    fill_plan_info(*h, out);
+  });
+}
+
+int tafv_gpu_get_plan_lists(tafv_gpu* h, int32_t* tau_out, int32_t* cad_out, int32_t* cells_flat,
+                            int32_t* faces_flat, int32_t* fringe_flat) {
+  return guard(h, [&] {
+    require(h->has_plan, "get_plan_lists: no plan");
+    std::vector<int8_t> tau(h->N), cad(h->F);
+    CK(cudaMemcpy(tau.data(), h->tau, h->N, cudaMemcpyDeviceToHost));
+    if (h->F) CK(cudaMemcpy(cad.data(), h->cad, h->F, cudaMemcpyDeviceToHost));
+    if (tau_out)
+      for (int i = 0; i < h->N; ++i) tau_out[h->cperm[i]] = tau[i];
+    if (cad_out)
+      for (int j = 0; j < h->F; ++j) cad_out[h->fperm[j]] = cad[j];
+    const int L = h->theta + 1;
+    // Device lists (internal ids, level-sorted) -> original ids, ascending per level.
+    auto export_list = [&](const int* dlist, long long n_total, const long long* counts,
+                           const std::vector<int>& perm, int32_t* out) {
+      std::vector<int> lst(n_total);
+      if (n_total) CK(cudaMemcpy(lst.data(), dlist, n_total * sizeof(int), cudaMemcpyDeviceToHost));
+      long long o = 0;
+      for (int l = 0; l < L; ++l) {
+        for (long long i = o; i < o + counts[l]; ++i) out[i] = perm[lst[i]];
+        std::sort(out + o, out + o + counts[l]);
+        o += counts[l];
+      }
+    };
+    long long nc = 0, nf = 0;
+    for (int l = 0; l < L; ++l) {
+      nc += h->ccount[l];
+      nf += h->fcount[l];
+    }
+    if (cells_flat) export_list(h->clist, nc, h->ccount, h->cperm, cells_flat);
+    if (faces_flat) export_list(h->flist, nf, h->fcount, h->fperm, faces_flat);
+    if (fringe_flat) {
+      // fringe[l]: cells of level l+1 flagged by a level-l face neighbour
+      // (levels.cpp:139-153), from the device flags.
+      std::vector<uint8_t> flag(h->N);
+      CK(cudaMemcpy(flag.data(), h->fflag, h->N, cudaMemcpyDeviceToHost));
+      std::vector<std::vector<int>> fr(std::max(0, h->theta));
+      for (int i = 0; i < h->N; ++i)
+        if (flag[i] && tau[i] > 0 && tau[i] - 1 < h->theta) fr[tau[i] - 1].push_back(h->cperm[i]);
+      long long o = 0;
+      for (auto& v : fr) {
+        std::sort(v.begin(), v.end());
+        std::copy(v.begin(), v.end(), fringe_flat + o);
+        o += (long long)v.size();
+      }
+    }
+  });
+}
+
+int tafv_gpu_run_iteration(tafv_gpu* h, tafv_record* out) {
+  return guard(h, [&] {
+    h->launches = 0;
+    h->ms[0] = h->ms[1] = h->ms[2] = 0;
+    run_iteration(*h, out);
+  });
+}
+
+int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* out) {
+  return guard(h, [&] {
+    require(opt != nullptr, "iterate: null options");
+    require(n >= 0, "integrate: negative iteration count");
+    h->launches = 0;
+    h->ms[0] = h->ms[1] = h->ms[2] = 0;
+    for (int i = 0; i < n; ++i) {
+      plan(*h, *opt);
+      run_iteration(*h, out ? out + i : nullptr);
+    }
+  });
+}
+
+int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* last) {
+  return guard(h, [&] {
+    require(opt != nullptr, "advance: null options");
+    require(n >= 0, "integrate: negative iteration count");
+    h->launches = 0;
+    h->ms[0] = h->ms[1] = h->ms[2] = 0;
+    for (int i = 0; i < n; ++i) {
+      plan(*h, *opt);
+      run_iteration(*h, i == n - 1 ? last : nullptr);
+    }
+  });
+}
+
+int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
+  return guard(h, [&] {
+    require(name && out, "get_array: null argument");
+    const std::string n = name;
+    auto rows = [&](const double* src, int count, int width, const int* dperm) {
+      const size_t total = (size_t)count * width;
+      double* stage = h->staging(total);
+      k_scatter_rows<<<h->grid_for((long long)total, 256), 256, 0, h->st>>>(src, dperm, count, width, stage);
+      CK(cudaMemcpyAsync(out, stage, total * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+    };
+    if (n == "w") rows(h->w, h->N, h->nv, h->d_cperm);
+    else if (n == "W") rows(h->W, h->N, h->nv, h->d_cperm);
+    else if (n == "w_pred") rows(h->wp, h->N, h->nv, h->d_cperm);
+    else if (n == "grad") rows(h->grad, h->N, h->nv * 3, h->d_cperm);
+    else if (n == "dt_max") rows(h->dtmax, h->N, 1, h->d_cperm);
+    else if (n == "phi_pred") rows(h->phi, h->F, h->nv, h->d_fperm);
+    else if (n == "int_substep") rows(h->isub, h->F, h->nv, h->d_fperm);
+    else if (n == "int_window") rows(h->iwin, h->F, h->nv, h->d_fperm);
+    else if (n == "raw_level" || n == "tau") {
+      std::vector<int8_t> v(h->N);
+      CK(cudaMemcpy(v.data(), n == "tau" ? h->tau : h->raw, h->N, cudaMemcpyDeviceToHost));
+      int32_t* o = static_cast<int32_t*>(out);
+      for (int i = 0; i < h->N; ++i) o[h->cperm[i]] = v[i];
+    } else {
+      require(false, "get_array: unknown array");
+    }
+  });
+}
+
+int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
+  return guard(h, [&] {
+    const std::string n = name ? name : "";
+    if (n == "grid_cap") h->grid_cap = (int)std::max<int64_t>(1, value);
+    else require(false, "set_flag: unknown flag");
+  });
+}
+
+int tafv_gpu_stats(tafv_gpu* h, int64_t* launches, double* ms3) {
+  if (!h) return TAFV_EINVAL;
+  if (launches) *launches = h->launches;
+  if (ms3)
+    for (int i = 0; i < 3; ++i) ms3[i] = h->ms[i];
+  return TAFV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+"""3D hexahedral meshes for the BASELINE.json configs (tafv_mesh_hex).
+
+The reference generator is 1D/2D only (proj/core/src/mesh.cpp:302-317); this
+is the 3D generator the configs need. It returns the canonical mesh dict
+(reference Mesh layout, Vec3) that the GPU solver and the CPU oracle both
+consume unchanged.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def hex_mesh(x, y, z, jitter=0.0, seed=0, permute=False):
+    """Tensor-product hex mesh on node coordinates x[nx+1], y[ny+1], z[nz+1]."""
+    L = N.lib()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    nx, ny, nz = len(x) - 1, len(y) - 1, len(z) - 1
+    nc, nf = C.c_int32(), C.c_int32()
+    rc = L.tafv_mesh_hex(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), float(jitter), int(seed) & (2**64 - 1),
+                         int(bool(permute)), C.byref(nc), C.byref(nf), *([None] * 9))
+    if rc != 0:
+        raise ValueError("tafv_mesh_hex: invalid spec")
+    nc, nf = nc.value, nf.value
+    m = {
+        "dim": 3,
+        "vol": np.empty(nc), "cen": np.empty((nc, 3)), "chl": np.empty(nc),
+        "fl": np.empty(nf, dtype=np.int32), "fr": np.empty(nf, dtype=np.int32),
+        "fp": np.empty(nf, dtype=np.int32), "fn": np.empty((nf, 3)), "fa": np.empty(nf),
+        "fc": np.empty((nf, 3)),
+    }
+    rc = L.tafv_mesh_hex(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), float(jitter), int(seed) & (2**64 - 1),
+                         int(bool(permute)), C.byref(C.c_int32()), C.byref(C.c_int32()),
+                         *[_ptr(m[k]) for k in ("vol", "cen", "chl", "fl", "fr", "fp", "fn", "fa", "fc")])
+    if rc != 0:
+        raise ValueError("tafv_mesh_hex: invalid spec")
+    return m
+
+
+def uniform_nodes(n):
+    return np.linspace(0.0, 1.0, n + 1)
+
+
+def geometric_nodes(n, ratio):
+    """Spacing multiplied by `ratio` per cell away from 0, normalised to [0, 1]."""
+    h = ratio ** np.arange(n, dtype=np.float64)
+    x = np.concatenate([[0.0], np.cumsum(h)])
+    x /= x[-1]
+    x[-1] = 1.0
+    return x
+
+
+def centre_graded_nodes(n, ratio, core):
+    """Symmetric grading: spacing 1 inside |u - 0.5| < core, growing
+    geometrically by `ratio` per cell outside (fine centre, coarse walls)."""
+    half = n // 2
+    h = np.ones(n)
+    u = (np.arange(n) + 0.5) / n - 0.5
+    k = np.maximum(0, np.abs(u) - core) * n  # cells beyond the core
+    h = ratio ** k
+    x = np.concatenate([[0.0], np.cumsum(h)])
+    x /= x[-1]
+    x[-1] = 1.0
+    del half
+    return x
