@@ -1,0 +1,353 @@
+#!/usr/bin/env python3
+"""Benchmark: FP64 Euler LTS finite-volume iterations, cell-updates/s.
+
+Contract (see task/README): one JSON line on rank 0.
+
+* A "step" is one global LTS iteration (plan_iteration + 2^theta
+  subiterations + trailing corrector, reference.cpp:89-129) over the
+  BASELINE config-2 workload (1M-cell jittered, graded, permuted hex mesh,
+  spherical blast, 3 temporal levels; configs[1] of BASELINE.json).
+* metric = cell-updates/s = sum over timed steps of C_eff / device time, with
+  C_eff = sum_tau 2^(theta-tau) |Omega(tau)| (the paper's level cost,
+  levels.cpp:68-79).
+* value: state resident in HBM, the whole timed region bracketed by CUDA
+  events on the library's stream (host plan read-backs included).
+* e2e: the same metric through the C ABI with HOST buffers: every step
+  uploads w, W from pinned memory, runs one iteration and downloads w, W.
+* roofline: the dominant kernel's algorithmic bytes / its event-timed
+  duration vs MEASURED_PEAKS.json hbm_gbs; roofline_iteration: BASELINE.md's
+  whole-iteration byte contract B_iter = 1220 C_eff + 568 F_eff + 312 R_eff.
+* cpu_baseline: the CPU oracle port (oracle/, test infra) on the same mesh,
+  all host threads, a bounded 2-iteration sample.
+* --impl reference: the oracle port alone (the reference's own CPU path
+  cannot run Euler 3D: proj/core is scalar 2D only), same config/metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec (FP64 Euler, adaptive levels)"
+UNIT = "cell-updates/s"
+
+# Algorithmic bytes per item of each kernel kind:
+# bytes that must cross HBM at least once per launch with perfect reuse.
+#   K1 per active cell: staged state 40, tau 1, CSR offset 4, 6 slots x 8,
+#      volume 8, centroid 24, gradient write 120;  per active face: normal+area
+#      32 + centroid 24;  per fringe cell: w and w_pred 80 + tau 1.
+#   K2 per active face: left/right 8, normal+area 32, centroid 24, cadence 1,
+#      pred: phi write 40 + window reset 40; corr: phi read 40 + window
+#      read/write 80 + substep write 40;  per touched cell (active + fringe):
+#      state 40, gradient 120, centroid 24, tau 1 (fringe +40 for the 2nd state).
+#   K3 per active cell: tau 1, offset 4, 6 face ids x 4, volume 8, W 40,
+#      pred: w_pred write 40; corr: W + w writes 80;  per active face: flux 40
+#      + cadence 1.
+def kernel_bytes(kind, cells, faces, fringe, slots_per_cell):
+    slot_b = slots_per_cell
+    if kind == "K1_grad_limit":
+        return cells * (40 + 1 + 4 + 8 * slot_b + 8 + 24 + 120) + faces * 56 + fringe * 81
+    if kind == "K2_face_pred":
+        return faces * (8 + 32 + 24 + 80) + cells * 185 + fringe * 225
+    if kind == "K2_face_corr":
+        return faces * (8 + 32 + 24 + 1 + 160) + cells * 185 + fringe * 225
+    if kind == "K3_update_pred":
+        return cells * (1 + 4 + 4 * slot_b + 8 + 40 + 40) + faces * 40
+    if kind == "K3_update_corr":
+        return cells * (1 + 4 + 4 * slot_b + 8 + 40 + 80) + faces * 41
+    return 0
+
+
+def c_eff(rec):
+    th = rec["theta"]
+    return sum(n << (th - l) for l, n in enumerate(rec["level_cells"]))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, device=0, period=0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_r(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_oracle_rate(mesh, w0, cfg, iterations, threads):
+    """Oracle port (test infra) on the host: cell-updates/s over `iterations`."""
+    from oracle import OracleSolver
+    o = OracleSolver(mesh, "euler", threads=threads)
+    o.init_values(w0.reshape(-1))
+    o.set_options(cfg.theta_max, cfg.cfl, cfg.dt_cap)
+    t = time.perf_counter()
+    recs = o.integrate(iterations)
+    dt = time.perf_counter() - t
+    return sum(c_eff(r) for r in recs) / dt, dt, recs
+
+
+def traffic_from_profiles(kind):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(kind)
+    if not e:
+        return None, None
+    return e.get("bytes_per_launch"), e.get("source")
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle port (all host threads), rank 0 only."""
+    if rank != 0:
+        return
+    from paper_1704_01144_b200 import configs
+    cfg = configs.get(args.config)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    threads = os.cpu_count() or 1
+    from oracle import OracleSolver
+    o = OracleSolver(mesh, "euler", threads=threads)
+    o.init_values(w0.reshape(-1))
+    o.set_options(cfg.theta_max, cfg.cfl, cfg.dt_cap)
+    o.integrate(args.warmup)
+    t = time.perf_counter()
+    recs = o.integrate(args.steps)
+    dt = time.perf_counter() - t
+    v = sum(c_eff(r) for r in recs) / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config generator)",
+        "config": {"workload": cfg.name, "cells": cfg.n_cells, "theta_max": cfg.theta_max,
+                   "cfl": cfg.cfl},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} global iterations of {cfg.name} after {args.warmup} "
+                                   "warm-up, oracle/tafv_oracle.cpp Euler port (the reference library "
+                                   "proj/core is scalar-2D only and cannot run this config)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+
+    from paper_1704_01144_b200 import Solver, configs
+    cfg = configs.get(args.config)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    s = Solver(mesh, "euler", device=local)
+    s.set_state(w0)
+    minfo = s.mesh_info()
+    slots_per_cell = minfo["adj_slots"] / minfo["n_cells"]
+
+    # warm-up (untimed): W global iterations
+    s.reference_integrate(opt, args.warmup)
+
+    # timed region: K iterations, device-resident state
+    s.set_flag("kernel_timing", 1)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        recs = s.reference_integrate(opt, args.steps)
+    torch.cuda.synchronize()
+    st = s.stats()
+    ms = st["ms_total"]
+    launches = st["launches"]
+    kt = s.kernel_times()
+    s.set_flag("kernel_timing", 0)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ceff = sum(c_eff(r) for r in recs)
+    value = ceff * world / (ms / 1e3)
+
+    # e2e: host buffers through the C ABI, copies inside every step
+    n = len(mesh["vol"])
+    pin_w = torch.from_numpy(w0.copy()).pin_memory()
+    pin_W = torch.from_numpy((w0 * mesh["vol"][:, None]).copy()).pin_memory()
+    out_w = torch.empty((n, 5), dtype=torch.float64).pin_memory()
+    out_W = torch.empty((n, 5), dtype=torch.float64).pin_memory()
+    e2e_ceff, e2e_t = 0, 0.0
+    lib = s.lib
+    import ctypes as C
+
+    from paper_1704_01144_b200 import _native as N
+    copt = opt.c()
+    rec = (N.Record * 1)()
+    t0c, itc = C.c_double(), C.c_int32()
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        s._c(lib.tafv_gpu_set_state(s.h, C.c_void_p(pin_w.data_ptr()), C.c_void_p(pin_W.data_ptr()), 0.0, 0))
+        s._c(lib.tafv_gpu_iterate(s.h, C.byref(copt), 1, rec))
+        s._c(lib.tafv_gpu_get_state(s.h, C.c_void_p(out_w.data_ptr()), C.c_void_p(out_W.data_ptr()),
+                                    C.byref(t0c), C.byref(itc)))
+        el = time.perf_counter() - t
+        if i > 0:  # first call warms the staging buffers
+            e2e_t += el
+            e2e_ceff += c_eff(rec[0].as_dict())
+    e2e = e2e_ceff * world / e2e_t
+    bytes_state = n * 5 * 8 * 2
+
+    # roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    kinds = [k for k in kt if k != "plan" and kt[k]["launches"] > 0]
+    dom = max(kinds, key=lambda k: kt[k]["ms"])
+    d = kt[dom]
+    bytes_dom = kernel_bytes(dom, d["cells"], d["faces"], d["fringe"], slots_per_cell)
+    achieved = bytes_dom / (d["ms"] / 1e3) / 1e9
+    traffic, traffic_src = traffic_from_profiles(dom)
+    per_launch_bytes = bytes_dom / d["launches"]
+    breakdown = {}
+    total_kernel_ms = sum(kt[k]["ms"] for k in kt)
+    for k, v in kt.items():
+        b = kernel_bytes(k, v["cells"], v["faces"], v["fringe"], slots_per_cell)
+        breakdown[k] = {"ms": round(v["ms"], 4), "launches": v["launches"],
+                        "share": round(v["ms"] / ms, 4) if ms else None,
+                        "GBps": round(b / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 and b else None}
+
+    # BASELINE.md whole-iteration byte contract (needs F_eff, R_eff per iteration)
+    # F_eff/R_eff come from the plans of the timed iterations: re-derive with the
+    # per-kind item counts (faces over predictor K2 launches = sum F_l per phase).
+    f_eff = kt["K2_face_pred"]["faces"]
+    r_eff = kt["K1_grad_limit"]["fringe"]
+    b_iter = 1220 * ceff + 568 * f_eff + 312 * r_eff
+    frac_iter = b_iter / (ms / 1e3) / (peak * 1e9)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v_cpu, dt_cpu, _ = cpu_oracle_rate(mesh, w0, cfg, 2, threads)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"2 global iterations of {cfg.name} from the initial state ({dt_cpu:.1f} s), "
+                         "oracle/tafv_oracle.cpp Euler port, contiguous-chunk thread pool"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded config generator: jittered/graded/permuted hex mesh, blast)",
+            "config": {"workload": cfg.name, "cells": int(n), "faces": int(len(mesh["fa"])),
+                       "theta_max": cfg.theta_max, "cfl": cfg.cfl,
+                       "levels_first_timed": recs[0]["level_cells"],
+                       "levels_last_timed": recs[-1]["level_cells"],
+                       "iterations": f"{args.warmup + 1}..{args.warmup + args.steps} of the run",
+                       "l2": "inputs larger than L2 (~1 GB working set vs 126 MB L2); no flush",
+                       "parallelism": f"dp{world}" if world > 1 else "single GPU"},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
+                    "d2h_bytes_per_step": bytes_state,
+                    "how": "tafv_gpu_set_state(pinned w,W) + tafv_gpu_iterate(1) + tafv_gpu_get_state; "
+                           "host wall clock per step"},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": round(per_launch_bytes),
+                         "peak_source": peak_src},
+            "roofline_iteration": {"model": "BASELINE.md B_iter = 1220 C_eff + 568 F_eff + 312 R_eff",
+                                   "c_eff": ceff, "f_eff": f_eff, "r_eff": r_eff,
+                                   "achieved_GBps": round(b_iter / (ms / 1e3) / 1e9, 1),
+                                   "frac": round(frac_iter, 4)},
+            "kernels": breakdown,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

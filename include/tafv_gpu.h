@@ -50,7 +50,7 @@ enum { TAFV_ADVECTION = 0, TAFV_BURGERS = 1, TAFV_EULER = 2 };
  * tafv_gpu_create in ascending original face id, exactly as the reference
  * builds it, and geometric closure is checked (mesh.cpp:273-284). */
 typedef struct tafv_mesh_view {
-  int32_t dim;                      /* 2 (scalar reference meshes) or 3 */
+  int32_t dim;                      /* 1 or 2 (scalar reference meshes) or 3 */
   int32_t n_cells;
   int32_t n_faces;
   const double* cell_volume;        /* [n_cells]    Cell::volume */
@@ -169,14 +169,27 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
  * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32). */
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
 
-/* Launch configuration knobs (bench/profiling): use_graph 0/1 captures each
- * theta's subiteration sweep as one CUDA graph (default 1). */
+/* Launch configuration knobs (bench/profiling):
+ *   "grid_cap"       max blocks per grid-stride launch;
+ *   "kernel_timing"  1: time every hot kernel with CUDA events on the
+ *                    library stream (resets the per-kind totals). */
 int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value);
 
 /* Kernel launches issued by the last run/iterate/advance call (own kernels
  * only), and device timings of the last call in milliseconds: [0] whole
  * call, [1] plan, [2] sweep (subiterations + trailing corrector). */
 int tafv_gpu_stats(tafv_gpu* h, int64_t* launches, double* ms3);
+
+/* Per-kind device time (ms), launch counts and processed items since
+ * kernel_timing was set: [0] K1 stage+gradient+limiter, [1] K2 face flux
+ * (predictor), [2] K2 face flux (corrector), [3] K3 gather+update
+ * (predictor), [4] K3 gather+update (corrector), [5] whole plan.
+ * items6x3[3k..3k+2] = active cells, active faces, fringe cells summed over
+ * kind k's launches (the inputs of the bench's algorithmic-byte model). */
+int tafv_gpu_kernel_times(tafv_gpu* h, double* ms6, int64_t* counts6, int64_t* items6x3);
+
+/* n_cells, n_faces, adjacency slots, nv of the uploaded mesh/physics. */
+int tafv_gpu_mesh_info(tafv_gpu* h, int64_t* info4);
 
 /* 3D hexahedral mesh generator (new: the reference generator is 1D/2D only,
  * mesh.cpp:302-317). Tensor-product node lattice x[nx+1], y[ny+1], z[nz+1],

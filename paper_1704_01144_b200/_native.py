@@ -103,7 +103,7 @@ EXPORTS = [
     "tafv_gpu_create", "tafv_gpu_destroy", "tafv_gpu_last_error", "tafv_gpu_set_state",
     "tafv_gpu_get_state", "tafv_gpu_plan", "tafv_gpu_inject_levels", "tafv_gpu_get_plan_lists",
     "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_get_array",
-    "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_mesh_hex",
+    "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex",
 ]
 
 _lib = None
@@ -133,6 +133,8 @@ def lib():
     L.tafv_gpu_get_array.argtypes = [vp, C.c_char_p, vp]
     L.tafv_gpu_set_flag.argtypes = [vp, C.c_char_p, i64]
     L.tafv_gpu_stats.argtypes = [vp, C.POINTER(i64), vp]
+    L.tafv_gpu_kernel_times.argtypes = [vp, vp, vp, vp]
+    L.tafv_gpu_mesh_info.argtypes = [vp, vp]
     L.tafv_mesh_hex.argtypes = [i32, i32, i32, vp, vp, vp, dbl, C.c_uint64, i32,
                                 C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
     _lib = L

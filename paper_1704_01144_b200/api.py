@@ -239,5 +239,21 @@ class Solver:
         self.lib.tafv_gpu_stats(self.h, C.byref(n), ms)
         return {"launches": n.value, "ms_total": ms[0], "ms_plan": ms[1], "ms_sweep": ms[2]}
 
+    KERNEL_KINDS = ("K1_grad_limit", "K2_face_pred", "K2_face_corr", "K3_update_pred",
+                    "K3_update_corr", "plan")
+
+    def kernel_times(self):
+        ms = (C.c_double * 6)()
+        n = (C.c_int64 * 6)()
+        it = (C.c_int64 * 18)()
+        self.lib.tafv_gpu_kernel_times(self.h, ms, n, it)
+        return {k: {"ms": ms[i], "launches": n[i], "cells": it[3 * i], "faces": it[3 * i + 1],
+                    "fringe": it[3 * i + 2]} for i, k in enumerate(self.KERNEL_KINDS)}
+
+    def mesh_info(self):
+        v = (C.c_int64 * 4)()
+        self.lib.tafv_gpu_mesh_info(self.h, v)
+        return {"n_cells": v[0], "n_faces": v[1], "adj_slots": v[2], "nv": v[3]}
+
     def set_flag(self, name, value):
         self._c(self.lib.tafv_gpu_set_flag(self.h, name.encode(), int(value)))

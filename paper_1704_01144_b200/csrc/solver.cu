@@ -111,7 +111,7 @@ struct tafv_gpu {
   PlanDev* hplan = nullptr;  // pinned
   double* stage_buf = nullptr;
   size_t stage_len = 0;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[6] = {};  // [0,1] sweep, [2,3] plan, [4,5] whole call
 
   // host copy of the plan
   bool has_plan = false;
@@ -121,6 +121,16 @@ struct tafv_gpu {
   double t0 = 0.0;
   int iteration = 0;
   bool state_set = false;
+
+  // per-kernel device timing (flag "kernel_timing"): event pairs around each
+  // hot launch, summed per kind after the call's host sync.
+  enum { kK1 = 0, kK2P, kK2C, kK3P, kK3C, kPlan, kNumKinds };
+  bool ktime = false;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<int> evkind;
+  double kms[kNumKinds] = {};
+  int64_t kcnt[kNumKinds] = {};
+  int64_t kitems[kNumKinds][3] = {};  // active cells, active faces, fringe cells per kind
 
   // stats
   int64_t launches = 0;
@@ -157,6 +167,7 @@ struct tafv_gpu {
     if (hplan) cudaFreeHost(hplan);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : evpool) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -167,7 +178,7 @@ namespace {
 void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   const int N = mv.n_cells, F = mv.n_faces;
   require(N > 0 && F >= 0, "mesh: empty mesh");
-  require(mv.dim == 2 || mv.dim == 3, "mesh: dim must be 2 or 3");
+  require(mv.dim >= 1 && mv.dim <= 3, "mesh: dim must be 1, 2 or 3");
   h.N = N;
   h.F = F;
   h.dim = mv.dim;
@@ -358,6 +369,40 @@ void alloc_state(tafv_gpu& h) {
   for (auto& e : h.ev) CK(cudaEventCreate(&e));
 }
 
+// ---- optional per-kernel timing ---------------------------------------------
+template <class F>
+void timed(tafv_gpu& h, int kind, F&& launch, long long cells = 0, long long faces = 0,
+           long long fringe = 0) {
+  if (!h.ktime) {
+    launch();
+    return;
+  }
+  h.kitems[kind][0] += cells;
+  h.kitems[kind][1] += faces;
+  h.kitems[kind][2] += fringe;
+  const size_t i = h.evkind.size();
+  while (h.evpool.size() < 2 * (i + 1)) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h.evpool.push_back(e);
+  }
+  CK(cudaEventRecord(h.evpool[2 * i], h.st));
+  launch();
+  CK(cudaEventRecord(h.evpool[2 * i + 1], h.st));
+  h.evkind.push_back(kind);
+}
+
+// After a host sync: fold the recorded pairs into the per-kind totals.
+void collect_times(tafv_gpu& h) {
+  for (size_t i = 0; i < h.evkind.size(); ++i) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h.evpool[2 * i], h.evpool[2 * i + 1]));
+    h.kms[h.evkind[i]] += ms;
+    h.kcnt[h.evkind[i]] += 1;
+  }
+  h.evkind.clear();
+}
+
 // ---- plan ------------------------------------------------------------------
 template <class P>
 void launch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
@@ -397,8 +442,18 @@ void finish_plan(tafv_gpu& h, int nkeys) {
     h.launches += 3;
   }
   CK(cudaGetLastError());
+  CK(cudaEventRecord(h.ev[3], h.st));
   CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
   CK(cudaStreamSynchronize(h.st));
+  {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h.ev[2], h.ev[3]));
+    h.ms[1] += ms;
+    if (h.ktime) {
+      h.kms[tafv_gpu::kPlan] += ms;
+      h.kcnt[tafv_gpu::kPlan] += 1;
+    }
+  }
   const PlanDev& p = *h.hplan;
   h.has_plan = false;
   if (p.err & 2) throw Error{TAFV_EINVAL, "level map: level outside [0, 15]"};
@@ -444,6 +499,7 @@ void plan(tafv_gpu& h, const tafv_options& opt) {
   require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
   require(h.state_set, "plan: state not set");
   h.has_plan = false;
+  CK(cudaEventRecord(h.ev[2], h.st));
   dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr);
   reset_plan_counts(h);
   k_classify<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.N, h.dtmax, h.dplan, opt.theta_max, h.raw);
@@ -480,6 +536,7 @@ void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options*
   }
   require(maxl < kMaxLevels, "level map: level above the supported 15");
   h.has_plan = false;
+  CK(cudaEventRecord(h.ev[2], h.st));
   CK(cudaMemsetAsync(h.dplan, 0, sizeof(PlanDev), h.st));
   int32_t* stage = reinterpret_cast<int32_t*>(h.staging(((size_t)h.N + 1) / 2));
   CK(cudaMemcpyAsync(stage, tau_host, (size_t)h.N * sizeof(int32_t), cudaMemcpyHostToDevice, h.st));
@@ -512,23 +569,34 @@ void phase(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const MeshDev md = h.mesh_dev();
   const StateDev sd = h.state_dev();
   const int gc = h.grid_for(na, 128), gf = h.grid_for(nf, 128);
+  const long long nfr = level < h.theta ? h.frcount[level] : 0;
   if (na > 0) {
-    k_grad_limit<P><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, front, pred ? 1 : 0);
+    timed(h, tafv_gpu::kK1, [&] {
+      k_grad_limit<P><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, front, pred ? 1 : 0);
+    }, na, nf, nfr);
     ++h.launches;
   }
   if (nf > 0) {
-    if (pred) k_face_flux<P, true><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
-    else k_face_flux<P, false><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
+    timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
+      if (pred) k_face_flux<P, true><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
+      else k_face_flux<P, false><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
+    }, na, nf, nfr);
     ++h.launches;
   }
   if (last) {
-    k_gather_update<P, false, true><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, h.N, h.dt, h.dplan,
-                                                                   h.partials);
+    timed(h, tafv_gpu::kK3C, [&] {
+      k_gather_update<P, false, true><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, h.N, h.dt,
+                                                                     h.dplan, h.partials);
+    }, h.N, h.F, 0);
     k_totals<<<1, 256, 0, h.st>>>(h.partials, h.nblk_last, P::NV, h.dplan);
     h.launches += 2;
   } else if (na > 0) {
-    if (pred) k_gather_update<P, true, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
-    else k_gather_update<P, false, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+    timed(h, pred ? tafv_gpu::kK3P : tafv_gpu::kK3C, [&] {
+      if (pred)
+        k_gather_update<P, true, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+      else
+        k_gather_update<P, false, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+    }, na, nf, 0);
     ++h.launches;
   }
 }
@@ -592,7 +660,23 @@ void run_iteration(tafv_gpu& h, tafv_record* rec) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
   h.ms[2] += ms;
+  collect_times(h);
   close_iteration(h, rec);
+}
+
+// Whole-call device time: events on the library stream bracket every
+// iteration, host syncs (the per-iteration plan read-back) included.
+template <class F>
+void timed_call(tafv_gpu& h, F&& body) {
+  h.launches = 0;
+  h.ms[0] = h.ms[1] = h.ms[2] = 0;
+  CK(cudaEventRecord(h.ev[4], h.st));
+  body();
+  CK(cudaEventRecord(h.ev[5], h.st));
+  CK(cudaEventSynchronize(h.ev[5]));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h.ev[4], h.ev[5]));
+  h.ms[0] = ms;
 }
 
 template <class F>
@@ -656,7 +740,7 @@ int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int
       default:
         require(false, "physics: unknown model");
     }
-    if (h->model != TAFV_EULER) require(mesh->dim == 2, "physics: scalar models run on 2D meshes");
+    if (h->model != TAFV_EULER) require(mesh->dim <= 2, "physics: scalar models run on 1D/2D meshes");
     else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
     upload_mesh(*h, *mesh);
     alloc_state(*h);
@@ -798,12 +882,12 @@ int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
   return guard(h, [&] {
     require(opt != nullptr, "iterate: null options");
     require(n >= 0, "integrate: negative iteration count");
-    h->launches = 0;
-    h->ms[0] = h->ms[1] = h->ms[2] = 0;
-    for (int i = 0; i < n; ++i) {
-      plan(*h, *opt);
-      run_iteration(*h, out ? out + i : nullptr);
-    }
+    timed_call(*h, [&] {
+      for (int i = 0; i < n; ++i) {
+        plan(*h, *opt);
+        run_iteration(*h, out ? out + i : nullptr);
+      }
+    });
   });
 }
 
@@ -811,12 +895,12 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
   return guard(h, [&] {
     require(opt != nullptr, "advance: null options");
     require(n >= 0, "integrate: negative iteration count");
-    h->launches = 0;
-    h->ms[0] = h->ms[1] = h->ms[2] = 0;
-    for (int i = 0; i < n; ++i) {
-      plan(*h, *opt);
-      run_iteration(*h, i == n - 1 ? last : nullptr);
-    }
+    timed_call(*h, [&] {
+      for (int i = 0; i < n; ++i) {
+        plan(*h, *opt);
+        run_iteration(*h, i == n - 1 ? last : nullptr);
+      }
+    });
   });
 }
 
@@ -853,9 +937,39 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
 int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
   return guard(h, [&] {
     const std::string n = name ? name : "";
-    if (n == "grid_cap") h->grid_cap = (int)std::max<int64_t>(1, value);
+    if (n == "grid_cap") {
+      h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+    } else if (n == "kernel_timing") {
+      h->ktime = value != 0;
+      for (int k = 0; k < tafv_gpu::kNumKinds; ++k) {
+        h->kms[k] = 0.0;
+        h->kcnt[k] = 0;
+        h->kitems[k][0] = h->kitems[k][1] = h->kitems[k][2] = 0;
+      }
+      h->evkind.clear();
+    }
     else require(false, "set_flag: unknown flag");
   });
+}
+
+int tafv_gpu_kernel_times(tafv_gpu* h, double* ms, int64_t* counts, int64_t* items) {
+  if (!h) return TAFV_EINVAL;
+  for (int k = 0; k < tafv_gpu::kNumKinds; ++k) {
+    if (ms) ms[k] = h->kms[k];
+    if (counts) counts[k] = h->kcnt[k];
+    if (items)
+      for (int j = 0; j < 3; ++j) items[3 * k + j] = h->kitems[k][j];
+  }
+  return TAFV_OK;
+}
+
+int tafv_gpu_mesh_info(tafv_gpu* h, int64_t* info4) {
+  if (!h || !info4) return TAFV_EINVAL;
+  info4[0] = h->N;
+  info4[1] = h->F;
+  info4[2] = h->M;
+  info4[3] = h->nv;
+  return TAFV_OK;
 }
 
 int tafv_gpu_stats(tafv_gpu* h, int64_t* launches, double* ms3) {
