@@ -42,10 +42,12 @@ constexpr int kMaxLevels = 16;
 struct MeshDev {
   int n_cells, n_faces;
   const double* __restrict__ vol;   // [N]
+  const double* __restrict__ ivol;  // [N] 1.0 / vol (host IEEE division == device)
   const double* __restrict__ cen;   // [N][3]
   const double* __restrict__ chl;   // [N]
   const int* __restrict__ adj_off;  // [N+1]
-  const int2* __restrict__ adj;     // [M] {face id (~f when the cell is the right side), neighbour}
+  const int* __restrict__ adj_face; // [M] face id (~f when the cell is the face's right side)
+  const int* __restrict__ adj_nb;   // [M] neighbour cell (-1 across transmissive faces)
   const int2* __restrict__ lr;      // [F] {left, resolved right (-1 transmissive)}
   const int* __restrict__ rcf;      // [F] face whose centroid the right side uses (periodic), or null
   const double4* __restrict__ geo;  // [F] {nx, ny, nz, area}
@@ -72,6 +74,8 @@ struct PlanDev {
   long long face_count[kMaxLevels];
   long long fringe_count[kMaxLevels];
   double totals[8];     // sum of W per component after the last iteration
+  int ncell_prefix[kMaxLevels];  // |{c : tau_c <= l}|: active cells of subiteration level l
+  int nface_prefix[kMaxLevels];  // |{f : cadence_f <= l}|
 };
 
 // ---- staging: pure function of the committed/predicted state ---------------
@@ -103,11 +107,45 @@ __device__ __forceinline__ void stage(const StateDev& s, int x, int tx, int fron
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
 __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
 
+// Barth-Jespersen update alpha = min(alpha, minmod(delta, head) / delta)
+// (kernels.cpp:111-117) with the division evaluated only where its value can
+// matter. Exactly equivalent, including signed zeros and NaN:
+//   same-sign, |head| >= |delta|  -> delta/delta = 1 (or NaN for inf/inf):
+//                                    smin(alpha <= 1, .) leaves alpha unchanged;
+//   opposite sign / zero / NaN head -> 0.0/delta = +-0 by the sign of delta;
+//   delta NaN                      -> NaN ratio: smin leaves alpha unchanged;
+//   delta == 0                     -> skipped by the reference.
+__device__ __forceinline__ double bj_update(double alpha, double delta, double head) {
+  if (delta > 0.0) {
+    if (head > 0.0) {
+      if (head < delta) alpha = smin(alpha, head / delta);
+    } else {
+      alpha = smin(alpha, 0.0);
+    }
+  } else if (delta < 0.0) {
+    if (head < 0.0) {
+      if (delta < head) alpha = smin(alpha, head / delta);
+    } else {
+      alpha = smin(alpha, -0.0);
+    }
+  }
+  return alpha;
+}
+
 // ---- K1: stage + Green-Gauss + Barth-Jespersen ----------------------------
-template <class P>
-__global__ void __launch_bounds__(128) k_grad_limit(MeshDev m, StateDev s, const int* __restrict__ list,
-                                                    int n, int front, int pred) {
+// Thread per cell, all NV components in registers (measured faster than a
+// component-parallel layout, which multiplies the shared index/geometry
+// instructions by NV). Per component the arithmetic is the reference's, slot
+// by slot in CSR order. DEG = 6 is the hex fast path (implicit offsets, fully
+// unrolled slot loop); DEG = 0 reads the CSR offsets. The active count comes
+// from device memory so the launch is graph-capturable.
+template <class P, int DEG>
+__global__ void __launch_bounds__(128, 4) k_grad_limit(MeshDev m, StateDev s,
+                                                    const int* __restrict__ list,
+                                                    const int* __restrict__ n_dev, int front,
+                                                    int pred) {
   constexpr int NV = P::NV, D = P::DIM;
+  const int n = *n_dev;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int c = list ? list[i] : i;
@@ -119,21 +157,22 @@ __global__ void __launch_bounds__(128) k_grad_limit(MeshDev m, StateDev s, const
     for (int k = 0; k < NV; ++k) {
 #pragma unroll
       for (int d = 0; d < D; ++d) g[k][d] = 0.0;
-      wmin[k] = __longlong_as_double(0x7ff0000000000000ll);   // +inf
-      wmax[k] = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
+      wmin[k] = __longlong_as_double(0x7ff0000000000000ll);
+      wmax[k] = __longlong_as_double((long long)0xfff0000000000000ull);
     }
     bool any = false;
-    const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
+    const int s0 = DEG ? DEG * c : m.adj_off[c];
+    const int s1 = DEG ? s0 + DEG : m.adj_off[c + 1];
+#pragma unroll
     for (int t = s0; t < s1; ++t) {
-      const int2 e = m.adj[t];
-      const int f = slot_face(e.x);
+      const int ef = m.adj_face[t], nb = m.adj_nb[t];
+      const int f = slot_face(ef);
       const double4 gm = m.geo[f];
-      const double scale = slot_sign(e.x) * gm.w;
-      const double nrm[3] = {gm.x, gm.y, gm.z};
+      const double scale = slot_sign(ef) * gm.w;
       double wf[NV];
-      if (e.y >= 0) {
+      if (nb >= 0) {
         double wn[NV];
-        stage<NV>(s, e.y, s.tau[e.y], front, pred, wn);
+        stage<NV>(s, nb, s.tau[nb], front, pred, wn);
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           wf[k] = 0.5 * (we[k] + wn[k]);
@@ -146,33 +185,35 @@ __global__ void __launch_bounds__(128) k_grad_limit(MeshDev m, StateDev s, const
         for (int k = 0; k < NV; ++k) wf[k] = we[k];
       }
 #pragma unroll
-      for (int k = 0; k < NV; ++k)
-#pragma unroll
-        for (int d = 0; d < D; ++d) g[k][d] += wf[k] * nrm[d] * scale;
+      for (int k = 0; k < NV; ++k) {
+        g[k][0] += wf[k] * gm.x * scale;
+        g[k][1] += wf[k] * gm.y * scale;
+        if (D == 3) g[k][D - 1] += wf[k] * gm.z * scale;
+      }
     }
-    const double inv_v = 1.0 / m.vol[c];
+    const double inv_v = m.ivol[c];
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
       for (int d = 0; d < D; ++d) g[k][d] = g[k][d] * inv_v;
     if (any) {
-      const double cc[3] = {m.cen[3 * (size_t)c], m.cen[3 * (size_t)c + 1], m.cen[3 * (size_t)c + 2]};
+      const double* cp = m.cen + 3 * (size_t)c;
+      const double cc0 = cp[0], cc1 = cp[1], cc2 = cp[2];
       double alpha[NV];
 #pragma unroll
       for (int k = 0; k < NV; ++k) alpha[k] = 1.0;
-      for (int t = s0; t < s1; ++t) {
-        const int f = slot_face(m.adj[t].x);
-        const double* fc = m.fcen + 3 * (size_t)f;
-        double dx[3];
 #pragma unroll
-        for (int d = 0; d < D; ++d) dx[d] = fc[d] - cc[d];
+      for (int t = s0; t < s1; ++t) {
+        const int f = slot_face(m.adj_face[t]);
+        const double* fc = m.fcen + 3 * (size_t)f;
+        const double dx0 = fc[0] - cc0, dx1 = fc[1] - cc1, dx2 = fc[2] - cc2;
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
-          double delta = g[k][0] * dx[0] + g[k][1] * dx[1];
-          if (D == 3) delta = delta + g[k][D - 1] * dx[D - 1];
+          double delta = g[k][0] * dx0 + g[k][1] * dx1;
+          if (D == 3) delta = delta + g[k][D - 1] * dx2;
           if (delta == 0.0) continue;
           const double head = delta > 0.0 ? wmax[k] - we[k] : wmin[k] - we[k];
-          alpha[k] = smin(alpha[k], minmod(delta, head) / delta);
+          alpha[k] = bj_update(alpha[k], delta, head);
         }
       }
 #pragma unroll
@@ -183,8 +224,9 @@ __global__ void __launch_bounds__(128) k_grad_limit(MeshDev m, StateDev s, const
     double* go = s.grad + (size_t)c * NV * 3;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d) go[3 * k + d] = d < D ? g[k][d < D ? d : 0] : 0.0;
+      go[3 * k] = g[k][0];
+      go[3 * k + 1] = g[k][1];
+      go[3 * k + 2] = D == 3 ? g[k][D - 1] : 0.0;
     }
   }
 }
@@ -201,9 +243,12 @@ __device__ __forceinline__ double extrapolate(double w, const double* g, const d
 // ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
 template <class P, bool PRED>
 __global__ void __launch_bounds__(128) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
-                                                   const int* __restrict__ list, int n, int front,
-                                                   double dt) {
+                                                   const int* __restrict__ list,
+                                                   const int* __restrict__ n_dev, int front,
+                                                   const PlanDev* __restrict__ plan) {
   constexpr int NV = P::NV, D = P::DIM;
+  const int n = *n_dev;
+  const double dt = plan->dt_min;
   const int stride = gridDim.x * blockDim.x;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int f = list ? list[i] : i;
@@ -295,57 +340,55 @@ __device__ __forceinline__ DD dd_merge(DD a, DD b) {
   return r;
 }
 
-template <class P, bool PRED, bool LAST>
+// Component-parallel like K1: lane k of a cell sums component k of the
+// signed face fluxes over the CSR slots in order, then updates its own
+// component. LAST (trailing corrector, identity list, all cells) also flags
+// non-finite w/W and leaves per-block, per-component compensated partial sums
+// of W (fixed shape => deterministic).
+template <class P, bool PRED, bool LAST, int DEG>
 __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
-                                                       const int* __restrict__ list, int n,
-                                                       double dt, PlanDev* plan, DD* partials) {
-  constexpr int NV = P::NV;
-  const int stride = gridDim.x * blockDim.x;
-  DD acc[LAST ? NV : 1];
+                                                       const int* __restrict__ list,
+                                                       const int* __restrict__ n_dev,
+                                                       PlanDev* plan, DD* partials) {
+  constexpr int NV = P::NV, CPW = 32 / NV;
+  const int n = *n_dev;
+  const double dt = plan->dt_min;
+  const int lane = threadIdx.x & 31;
+  const int j = lane / NV, k = lane - j * NV;
+  const bool lane_ok = j < CPW;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  DD acc{0.0, 0.0};
   bool bad = false;
-  if (LAST) {
+  if (lane_ok) {
+    for (int i = warp * CPW + j; i < n; i += nwarps * CPW) {
+      const int c = list ? list[i] : i;
+      const int tc = s.tau[c];
+      double sum = 0.0;
+      const int s0 = DEG ? DEG * c : m.adj_off[c];
+      const int s1 = DEG ? s0 + DEG : m.adj_off[c + 1];
 #pragma unroll
-    for (int k = 0; k < (LAST ? NV : 1); ++k) acc[k] = DD{0.0, 0.0};
-  }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int c = list ? list[i] : i;
-    const int tc = s.tau[c];
-    double sum[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) sum[k] = 0.0;
-    const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
-    for (int t = s0; t < s1; ++t) {
-      const int e = m.adj[t].x;
-      const int f = slot_face(e);
-      const double sg = slot_sign(e);
-      const double* ph;
-      if (PRED) ph = s.phi + (size_t)f * NV;
-      else ph = (tc > s.cad[f] ? s.iwin : s.isub) + (size_t)f * NV;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) sum[k] += sg * ph[k];
-    }
-    const double v = m.vol[c];
-    if (PRED) {
-      const double dtw = dt * (double)(1 << tc);
-      double* wp = s.wp + (size_t)c * NV;
-      const double* W = s.W + (size_t)c * NV;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const double Wp = W[k] + dtw * (-sum[k]);
-        wp[k] = Wp / v;
+      for (int t = s0; t < s1; ++t) {
+        const int e = m.adj_face[t];
+        const int f = slot_face(e);
+        const double* ph;
+        if (PRED) ph = s.phi;
+        else ph = tc > s.cad[f] ? s.iwin : s.isub;
+        sum += slot_sign(e) * ph[(size_t)f * NV + k];
       }
-    } else {
-      double* W = s.W + (size_t)c * NV;
-      double* w = s.w + (size_t)c * NV;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const double Wn = W[k] + (-sum[k]);
+      const size_t ci = (size_t)c * NV + k;
+      const double v = m.vol[c];
+      if (PRED) {
+        const double dtw = dt * (double)(1 << tc);
+        s.wp[ci] = (s.W[ci] + dtw * (-sum)) / v;
+      } else {
+        const double Wn = s.W[ci] + (-sum);
         const double wn = Wn / v;
-        W[k] = Wn;
-        w[k] = wn;
+        s.W[ci] = Wn;
+        s.w[ci] = wn;
         if (LAST) {
           bad = bad || !isfinite(Wn) || !isfinite(wn);
-          acc[k < (LAST ? NV : 1) ? k : 0] = dd_add(acc[k < (LAST ? NV : 1) ? k : 0], Wn);
+          acc = dd_add(acc, Wn);
         }
       }
     }
@@ -353,35 +396,33 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
   if (LAST) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) plan->nonfinite = 1;
     __shared__ DD red[128];
-#pragma unroll
-    for (int k = 0; k < (LAST ? NV : 1); ++k) {
-      red[threadIdx.x] = acc[k];
-      __syncthreads();
-      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
-        __syncthreads();
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.x < NV) {  // component k = threadIdx.x: its lanes, in thread order
+      DD a{0.0, 0.0};
+      for (int t = threadIdx.x; t < blockDim.x; ++t) {
+        const int l = t & 31, jj = l / NV;
+        if (jj < CPW && l - jj * NV == (int)threadIdx.x) a = dd_merge(a, red[t]);
       }
-      if (threadIdx.x == 0) partials[(size_t)k * gridDim.x + blockIdx.x] = red[0];
-      __syncthreads();
+      partials[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = a;
     }
   }
 }
 
-// Fixed-order reduction of the per-block partials (one block).
-__global__ void k_totals(const DD* partials, int nblocks, int nv, PlanDev* plan) {
+// Fixed-order reduction of the per-block partials: block k reduces
+// component k (deterministic tree over a fixed number of partials).
+__global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan) {
   __shared__ DD red[256];
-  for (int k = 0; k < nv; ++k) {
-    DD a{0.0, 0.0};
-    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a = dd_merge(a, partials[(size_t)k * nblocks + b]);
-    red[threadIdx.x] = a;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) plan->totals[k] = red[0].hi + red[0].lo;
+  const int k = blockIdx.x;
+  DD a{0.0, 0.0};
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a = dd_merge(a, partials[(size_t)k * nblocks + b]);
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
     __syncthreads();
   }
+  if (threadIdx.x == 0) plan->totals[k] = red[0].hi + red[0].lo;
 }
 
 // ---- plan kernels ----------------------------------------------------------
@@ -456,7 +497,7 @@ __global__ void k_smooth(MeshDev m, const int8_t* in, int8_t* out) {
     int bound = in[c];
     const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
     for (int t = s0; t < s1; ++t) {
-      const int nb = m.adj[t].y;
+      const int nb = m.adj_nb[t];
       if (nb >= 0) {
         const int v = in[nb] + 1;
         bound = v < bound ? v : bound;
@@ -587,6 +628,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(const int8_t* 
       running[threadIdx.x] += tot;
     }
     __syncthreads();
+  }
+}
+
+// Active-set sizes of every subiteration level (prefix sums of the per-level
+// counts) for the graph-captured sweep, which reads its counts on device.
+__global__ void k_plan_prefix(PlanDev* plan) {
+  if (threadIdx.x != 0) return;
+  long long c = 0, f = 0;
+  for (int l = 0; l < kMaxLevels; ++l) {
+    c += plan->cell_count[l];
+    f += plan->face_count[l];
+    plan->ncell_prefix[l] = (int)c;
+    plan->nface_prefix[l] = (int)f;
   }
 }
 

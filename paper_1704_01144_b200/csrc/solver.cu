@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -88,9 +89,19 @@ struct tafv_gpu {
   std::vector<double> vol_host;
 
   // device mesh
-  double *vol = nullptr, *cen = nullptr, *chl = nullptr, *fcen = nullptr;
+  double *vol = nullptr, *ivol = nullptr, *cen = nullptr, *chl = nullptr, *fcen = nullptr;
+  bool deg6 = false;  // every cell has exactly 6 CSR slots (hex meshes): fast path
+  // Launch shapes: grid-stride kernels with a fixed, occupancy-sized grid
+  // (graph mode) so the captured sweep of a theta never changes.
+  bool use_graph = true;
+  std::map<int, cudaGraphExec_t> graphs;  // theta -> instantiated sweep
+  std::map<int, int64_t> graph_launches;  // kernels inside each graph
+  bool capturing = false;
+  int grid_k1 = 0, grid_k2 = 0, grid_k3 = 0;
+  int plan_nkeys = 0;
   int* adj_off = nullptr;
-  int2* adj = nullptr;
+  int* adj_face = nullptr;  // [M] face id, ~f on the face's right side
+  int* adj_nb = nullptr;    // [M] neighbour cell or -1
   int2* lr = nullptr;
   int* rcf = nullptr;
   double4* geo = nullptr;
@@ -138,7 +149,7 @@ struct tafv_gpu {
   int grid_cap = 148 * 8;
 
   MeshDev mesh_dev() const {
-    return MeshDev{N, F, vol, cen, chl, adj_off, adj, lr, periodic ? rcf : nullptr, geo, fcen};
+    return MeshDev{N, F, vol, ivol, cen, chl, adj_off, adj_face, adj_nb, lr, periodic ? rcf : nullptr, geo, fcen};
   }
   StateDev state_dev() const { return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin}; }
 
@@ -159,7 +170,8 @@ struct tafv_gpu {
 
   ~tafv_gpu() {
     cudaSetDevice(device);
-    void* ptrs[] = {vol, cen, chl, fcen, adj_off, adj, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
+    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    void* ptrs[] = {vol, ivol, cen, chl, fcen, adj_off, adj_face, adj_nb, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
                     grad, phi, isub, iwin, tau, cad, raw, tmpa, tmpb, fflag, dtmax, blockmin,
                     cell_counts, face_counts, clist, flist, partials, dplan, stage_buf};
     for (void* p : ptrs)
@@ -247,18 +259,20 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   }
   for (int i = 0; i < N; ++i) off[i + 1] += off[i];
   h.M = off[N];
-  std::vector<int2> adj(h.M);
+  std::vector<int> adj_face(h.M), adj_nb(h.M);
   std::vector<double> sgn(h.M);
   {
     std::vector<int> cur(off.begin(), off.end() - 1);
     for (int f = 0; f < F; ++f) {
       const int rr = resolved_right(f);
       const int L = cinv[mv.face_left[f]];
-      adj[cur[L]] = make_int2(finv[f], rr >= 0 ? cinv[rr] : -1);
+      adj_face[cur[L]] = finv[f];
+      adj_nb[cur[L]] = rr >= 0 ? cinv[rr] : -1;
       sgn[cur[L]++] = 1.0;
       if (mv.face_right[f] >= 0) {
         const int R = cinv[mv.face_right[f]];
-        adj[cur[R]] = make_int2(~finv[f], L);
+        adj_face[cur[R]] = ~finv[f];
+        adj_nb[cur[R]] = L;
         sgn[cur[R]++] = -1.0;
       }
     }
@@ -267,7 +281,7 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   for (int i = 0; i < N; ++i) {
     double s[3] = {0.0, 0.0, 0.0};
     for (int t = off[i]; t < off[i + 1]; ++t) {
-      const int j = adj[t].x >= 0 ? adj[t].x : ~adj[t].x;
+      const int j = adj_face[t] >= 0 ? adj_face[t] : ~adj_face[t];
       const int f = h.fperm[j];
       for (int d = 0; d < 3; ++d) s[d] += sgn[t] * mv.face_normal[3 * (size_t)f + d] * mv.face_area[f];
     }
@@ -303,14 +317,22 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   };
   h.vol = dalloc<double>(N);
   up(h.vol, vol);
+  std::vector<double> ivol(N);
+  for (int i = 0; i < N; ++i) ivol[i] = 1.0 / vol[i];  // same IEEE quotient as the device's
+  h.ivol = dalloc<double>(N);
+  up(h.ivol, ivol);
+  h.deg6 = true;
+  for (int i = 0; i <= N && h.deg6; ++i) h.deg6 = off[i] == 6 * i;
   h.cen = dalloc<double>(3 * (size_t)N);
   up(h.cen, cen);
   h.chl = dalloc<double>(N);
   up(h.chl, chl);
   h.adj_off = dalloc<int>(N + 1);
   up(h.adj_off, off);
-  h.adj = dalloc<int2>(h.M);
-  up(h.adj, adj);
+  h.adj_face = dalloc<int>(h.M);
+  up(h.adj_face, adj_face);
+  h.adj_nb = dalloc<int>(h.M);
+  up(h.adj_nb, adj_nb);
   h.lr = dalloc<int2>(F);
   up(h.lr, lr);
   if (h.periodic) {
@@ -360,13 +382,39 @@ void alloc_state(tafv_gpu& h) {
   h.face_counts = dalloc<int>((size_t)std::max(1, h.ntile_f) * kMaxLevels);
   h.clist = dalloc<int>(N);
   h.flist = dalloc<int>(F);
-  h.nblk_last = h.grid_cap;
+  h.nblk_last = h.sms * 16;
   h.partials = dalloc<DD>((size_t)h.nblk_last * 8);
   h.dplan = dalloc<PlanDev>(1);
   CK(cudaMemset(h.dplan, 0, sizeof(PlanDev)));
   CK(cudaMallocHost(&h.hplan, sizeof(PlanDev)));
   std::memset(h.hplan, 0, sizeof(PlanDev));
   for (auto& e : h.ev) CK(cudaEventCreate(&e));
+}
+
+// Fixed grids for graph capture: every SM filled to the kernel's occupancy.
+template <class P, int DEG>
+void set_grids_t(tafv_gpu& h) {
+  int b1 = 0, b2 = 0, b3 = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_grad_limit<P, DEG>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_face_flux<P, true>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_gather_update<P, true, false, DEG>, 128, 0));
+  h.grid_k1 = h.sms * std::max(1, b1);
+  h.grid_k2 = h.sms * std::max(1, b2);
+  h.grid_k3 = h.sms * std::max(1, b3);
+}
+
+template <class P>
+void set_grids_p(tafv_gpu& h) {
+  if (h.deg6) set_grids_t<P, 6>(h);
+  else set_grids_t<P, 0>(h);
+}
+
+void set_grids(tafv_gpu& h) {
+  switch (h.model) {
+    case TAFV_ADVECTION: set_grids_p<Advection2D>(h); break;
+    case TAFV_BURGERS: set_grids_p<Burgers2D>(h); break;
+    default: set_grids_p<Euler3D>(h); break;
+  }
 }
 
 // ---- optional per-kernel timing ---------------------------------------------
@@ -421,13 +469,15 @@ void dispatch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_s
 }
 
 void reset_plan_counts(tafv_gpu& h) {
-  // Clear counts/flags but keep dt_min (written before by the dt kernels).
-  CK(cudaMemsetAsync(&h.dplan->err, 0, sizeof(int) * 2 + sizeof(long long) * 3 * kMaxLevels, h.st));
+  // Clear the error flags and counts; keep dt_min (written by the dt kernels)
+  // and nonfinite/totals (the previous sweep's, read back with this plan).
+  CK(cudaMemsetAsync(&h.dplan->err, 0, sizeof(int), h.st));
+  CK(cudaMemsetAsync(&h.dplan->cell_count[0], 0, sizeof(long long) * 3 * kMaxLevels, h.st));
 }
 
 // Face cadences, fringe counts and the level-sorted cell / face lists, then
-// the single host read-back of the plan.
-void finish_plan(tafv_gpu& h, int nkeys) {
+// the asynchronous read-back of the plan (and of the previous sweep's flags).
+void enqueue_finish_plan(tafv_gpu& h, int nkeys) {
   const MeshDev md = h.mesh_dev();
   CK(cudaMemsetAsync(h.fflag, 0, h.N, h.st));
   k_face_cadence<<<h.grid_for(h.F, 256), 256, 0, h.st>>>(md, h.tau, h.cad, h.fflag, h.dplan);
@@ -441,10 +491,16 @@ void finish_plan(tafv_gpu& h, int nkeys) {
     k_tile_scatter<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F, nkeys, h.face_counts, h.flist);
     h.launches += 3;
   }
+  k_plan_prefix<<<1, 32, 0, h.st>>>(h.dplan);
+  ++h.launches;
   CK(cudaGetLastError());
   CK(cudaEventRecord(h.ev[3], h.st));
   CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
-  CK(cudaStreamSynchronize(h.st));
+  h.plan_nkeys = nkeys;
+}
+
+// Host side of the plan once its read-back landed (after a stream sync).
+void accept_plan(tafv_gpu& h) {
   {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h.ev[2], h.ev[3]));
@@ -455,6 +511,7 @@ void finish_plan(tafv_gpu& h, int nkeys) {
     }
   }
   const PlanDev& p = *h.hplan;
+  const int nkeys = h.plan_nkeys;
   h.has_plan = false;
   if (p.err & 2) throw Error{TAFV_EINVAL, "level map: level outside [0, 15]"};
   if (p.err & 1)
@@ -494,7 +551,7 @@ void fill_plan_info(const tafv_gpu& h, tafv_plan_info* out) {
   out->cost_ratio = cost == 0 ? 1.0 : (double)((1ll << h.theta) * (long long)h.N) / (double)cost;
 }
 
-void plan(tafv_gpu& h, const tafv_options& opt) {
+void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
   require(opt.theta_max >= 0, "classify: theta_max must be >= 0");
   require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
   require(h.state_set, "plan: state not set");
@@ -519,12 +576,23 @@ void plan(tafv_gpu& h, const tafv_options& opt) {
       src = dst;
     }
   }
-  finish_plan(h, opt.theta_max + 1);
-  // reference.cpp:93
+  enqueue_finish_plan(h, opt.theta_max + 1);
+}
+
+// After the plan read-back: levels, counts and the stable-step check
+// (reference.cpp:93).
+void check_plan(tafv_gpu& h) {
+  accept_plan(h);
   if (!(std::isfinite(h.dt) && h.dt > 0.0)) {
     h.has_plan = false;
     throw Error{TAFV_EINVAL, "integrate: stable step collapsed"};
   }
+}
+
+void plan(tafv_gpu& h, const tafv_options& opt) {
+  enqueue_plan(h, opt);
+  CK(cudaStreamSynchronize(h.st));
+  check_plan(h);
 }
 
 void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options* opt) {
@@ -549,7 +617,9 @@ void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options*
     require(opt != nullptr, "inject_levels: dt <= 0 needs options for the stable step");
     dispatch_dt_max(h, opt->cfl, opt->dt_cap, h.tau);
   }
-  finish_plan(h, maxl + 1);
+  enqueue_finish_plan(h, maxl + 1);
+  CK(cudaStreamSynchronize(h.st));
+  accept_plan(h);
   if (!(std::isfinite(h.dt) && h.dt > 0.0)) {  // levels.cpp:54
     h.has_plan = false;
     throw Error{TAFV_EINVAL, "level map: dt must be positive"};
@@ -557,48 +627,58 @@ void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options*
 }
 
 // ---- the subiteration sweep ------------------------------------------------
-template <class P>
-void phase(tafv_gpu& h, bool pred, bool last, int level, int front) {
+template <class P, int DEG>
+void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   long long na = 0, nf = 0;
   for (int l = 0; l <= level; ++l) {
     na += h.ccount[l];
     nf += h.fcount[l];
   }
-  const int* cl = na == h.N ? nullptr : h.clist;
-  const int* fl = nf == h.F ? nullptr : h.flist;
+  // Level theta activates every cell and face (tau <= theta): identity lists.
+  const bool all = level == h.theta;
+  const int* cl = all ? nullptr : h.clist;
+  const int* fl = all ? nullptr : h.flist;
+  const int* ncp = &h.dplan->ncell_prefix[level];
+  const int* nfp = &h.dplan->nface_prefix[level];
   const MeshDev md = h.mesh_dev();
   const StateDev sd = h.state_dev();
-  const int gc = h.grid_for(na, 128), gf = h.grid_for(nf, 128);
+  // Graph mode: fixed occupancy-sized grids (the capture must not depend on
+  // the counts); direct mode: grids sized from the host-known counts.
+  const bool fixed = h.capturing;
+  constexpr int CPB = (32 / P::NV) * 4;  // cells per 128-thread block in K3
+  const int g1 = fixed ? h.grid_k1 : h.grid_for(na, 128);
+  const int g2 = fixed ? h.grid_k2 : h.grid_for(nf, 128);
+  const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
-  if (na > 0) {
-    timed(h, tafv_gpu::kK1, [&] {
-      k_grad_limit<P><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, front, pred ? 1 : 0);
-    }, na, nf, nfr);
-    ++h.launches;
-  }
-  if (nf > 0) {
-    timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
-      if (pred) k_face_flux<P, true><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
-      else k_face_flux<P, false><<<gf, 128, 0, h.st>>>(md, sd, h.pp, fl, (int)nf, front, h.dt);
-    }, na, nf, nfr);
-    ++h.launches;
-  }
+  timed(h, tafv_gpu::kK1, [&] {
+    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, cl, ncp, front, pred ? 1 : 0);
+  }, na, nf, nfr);
+  timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
+    if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan);
+    else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan);
+  }, na, nf, nfr);
   if (last) {
     timed(h, tafv_gpu::kK3C, [&] {
-      k_gather_update<P, false, true><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, h.N, h.dt,
-                                                                     h.dplan, h.partials);
-    }, h.N, h.F, 0);
-    k_totals<<<1, 256, 0, h.st>>>(h.partials, h.nblk_last, P::NV, h.dplan);
-    h.launches += 2;
-  } else if (na > 0) {
+      k_gather_update<P, false, true, DEG><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, ncp,
+                                                                          h.dplan, h.partials);
+    }, na, nf, 0);
+    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan);
+    h.launches += 4;
+  } else {
     timed(h, pred ? tafv_gpu::kK3P : tafv_gpu::kK3C, [&] {
       if (pred)
-        k_gather_update<P, true, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+        k_gather_update<P, true, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials);
       else
-        k_gather_update<P, false, false><<<gc, 128, 0, h.st>>>(md, sd, cl, (int)na, h.dt, h.dplan, h.partials);
+        k_gather_update<P, false, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials);
     }, na, nf, 0);
-    ++h.launches;
+    h.launches += 3;
   }
+}
+
+template <class P>
+void phase(tafv_gpu& h, bool pred, bool last, int level, int front) {
+  if (h.deg6) phase_t<P, 6>(h, pred, last, level, front);
+  else phase_t<P, 0>(h, pred, last, level, front);
 }
 
 template <class P>
@@ -613,7 +693,7 @@ void sweep(tafv_gpu& h) {
   phase<P>(h, false, true, h.theta, subs);  // trailing corrector, reference.cpp:121
 }
 
-void run_sweep(tafv_gpu& h) {
+void enqueue_sweep_direct(tafv_gpu& h) {
   CK(cudaMemsetAsync(&h.dplan->nonfinite, 0, sizeof(int), h.st));
   switch (h.model) {
     case TAFV_ADVECTION: sweep<Advection2D>(h); break;
@@ -623,8 +703,35 @@ void run_sweep(tafv_gpu& h) {
   CK(cudaGetLastError());
 }
 
-// Host side of the end of run_iteration (reference.cpp:123-128) once the
-// sweep's flags and totals are back on the host.
+// The whole 2^theta subiteration sweep as one CUDA graph per theta: every
+// launch reads its active count and dt from the device plan, so the graph
+// captured once replays for every later iteration with the same theta.
+void run_sweep(tafv_gpu& h) {
+  if (!h.use_graph || h.ktime) {
+    enqueue_sweep_direct(h);
+    return;
+  }
+  auto it = h.graphs.find(h.theta);
+  if (it == h.graphs.end()) {
+    cudaGraph_t g;
+    h.capturing = true;
+    const int64_t l0 = h.launches;
+    CK(cudaStreamBeginCapture(h.st, cudaStreamCaptureModeThreadLocal));
+    enqueue_sweep_direct(h);
+    const cudaError_t e = cudaStreamEndCapture(h.st, &g);
+    h.capturing = false;
+    CK(e);
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphDestroy(g));
+    it = h.graphs.emplace(h.theta, ex).first;
+    h.graph_launches[h.theta] = h.launches - l0;
+    h.launches = l0;
+  }
+  CK(cudaGraphLaunch(it->second, h.st));
+  h.launches += h.graph_launches[h.theta];
+}
+
 void close_iteration(tafv_gpu& h, tafv_record* rec) {
   if (h.hplan->nonfinite) {
     h.has_plan = false;
@@ -662,6 +769,50 @@ void run_iteration(tafv_gpu& h, tafv_record* rec) {
   h.ms[2] += ms;
   collect_times(h);
   close_iteration(h, rec);
+}
+
+// reference_integrate as a pipelined loop: the plan of iteration i+1 is
+// enqueued right behind sweep i and ONE read-back carries both plan i+1 and
+// sweep i's divergence flag and totals, so the host waits once per iteration.
+// Semantics match the sequential loop: iteration i's divergence is reported
+// before plan i+1's errors, and the state is left as the reference leaves it.
+void integrate_pipelined(tafv_gpu& h, const tafv_options& opt, int n, tafv_record* out,
+                         bool keep_all) {
+  if (n <= 0) return;
+  enqueue_plan(h, opt);
+  CK(cudaStreamSynchronize(h.st));
+  check_plan(h);
+  for (int i = 0; i < n; ++i) {
+    // snapshot the plan that drives sweep i (the next plan overwrites h.*)
+    const int theta = h.theta;
+    const double dt = h.dt;
+    long long cc[kMaxLevels];
+    std::memcpy(cc, h.ccount, sizeof cc);
+    run_sweep(h);
+    const bool more = i + 1 < n;
+    if (more) {
+      enqueue_plan(h, opt);
+    } else {
+      CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+    }
+    CK(cudaStreamSynchronize(h.st));
+    collect_times(h);
+    // close iteration i with its own plan
+    const int th_next = h.theta;
+    const double dt_next = h.dt;
+    long long cc_next[kMaxLevels];
+    std::memcpy(cc_next, h.ccount, sizeof cc_next);
+    h.theta = theta;
+    h.dt = dt;
+    std::memcpy(h.ccount, cc, sizeof cc);
+    close_iteration(h, (keep_all || !more) && out ? (keep_all ? out + i : out) : nullptr);
+    if (more) {
+      h.theta = th_next;
+      h.dt = dt_next;
+      std::memcpy(h.ccount, cc_next, sizeof cc_next);
+      check_plan(h);
+    }
+  }
 }
 
 // Whole-call device time: events on the library stream bracket every
@@ -744,6 +895,7 @@ int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int
     else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
     upload_mesh(*h, *mesh);
     alloc_state(*h);
+    set_grids(*h);
   } catch (const Error& e) {
     g_create_error = e.what;
     delete h;
@@ -882,12 +1034,7 @@ int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
   return guard(h, [&] {
     require(opt != nullptr, "iterate: null options");
     require(n >= 0, "integrate: negative iteration count");
-    timed_call(*h, [&] {
-      for (int i = 0; i < n; ++i) {
-        plan(*h, *opt);
-        run_iteration(*h, out ? out + i : nullptr);
-      }
-    });
+    timed_call(*h, [&] { integrate_pipelined(*h, *opt, n, out, true); });
   });
 }
 
@@ -895,12 +1042,7 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
   return guard(h, [&] {
     require(opt != nullptr, "advance: null options");
     require(n >= 0, "integrate: negative iteration count");
-    timed_call(*h, [&] {
-      for (int i = 0; i < n; ++i) {
-        plan(*h, *opt);
-        run_iteration(*h, i == n - 1 ? last : nullptr);
-      }
-    });
+    timed_call(*h, [&] { integrate_pipelined(*h, *opt, n, last, false); });
   });
 }
 
@@ -939,6 +1081,8 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     const std::string n = name ? name : "";
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+    } else if (n == "use_graph") {
+      h->use_graph = value != 0;
     } else if (n == "kernel_timing") {
       h->ktime = value != 0;
       for (int k = 0; k < tafv_gpu::kNumKinds; ++k) {

@@ -194,3 +194,30 @@ def test_divergence_detected(gpu):
     s.set_state(w0)
     with pytest.raises((Diverged, InvalidArgument)):
         s.reference_integrate(cfg.options(), 3)
+
+
+@pytest.mark.parametrize("use_graph", [0, 1])
+def test_graph_and_direct_launch_bitwise(use_graph, gpu):
+    """The CUDA-graph sweep and the direct-launch sweep both reproduce the
+    oracle bitwise (records included), through reference_integrate."""
+    from oracle import OracleSolver
+    cfg = configs.get(2, 5)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    g = Solver(mesh, "euler")
+    g.set_flag("use_graph", use_graph)
+    g.set_state(w0)
+    rg = g.reference_integrate(opt, 6)
+    o = OracleSolver(mesh, "euler", threads=8)
+    o.init_values(w0.reshape(-1))
+    o.set_options(opt.theta_max, opt.cfl, opt.dt_cap)
+    ro = o.integrate(6)
+    w, W, t0, it = g.get_state()
+    np.testing.assert_array_equal(w.reshape(-1), o.get("w"))
+    np.testing.assert_array_equal(W.reshape(-1), o.get("W"))
+    assert (t0, it) == o.time()
+    assert [r["dt"] for r in rg] == [r["dt"] for r in ro]
+    assert [r["level_cells"] for r in rg] == [r["level_cells"] for r in ro]
+    assert [r["iteration"] for r in rg] == [r["iteration"] for r in ro]
+    assert [r["t_start"] for r in rg] == [r["t_start"] for r in ro]
