@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtafv_gpu.so")
+# TAFV_GPU_LIB overrides the in-tree library (A/B of two builds in one run).
+LIB_PATH = os.environ.get("TAFV_GPU_LIB") or os.path.join(HERE, "libtafv_gpu.so")
 
 TAFV_OK, TAFV_EINVAL, TAFV_ELOGIC, TAFV_EDIVERGED, TAFV_ECUDA, TAFV_ENCCL = range(6)
 TAFV_ADVECTION, TAFV_BURGERS, TAFV_EULER = 0, 1, 2

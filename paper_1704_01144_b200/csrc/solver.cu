@@ -96,6 +96,10 @@ struct tafv_gpu {
   bool use_graph = true;
   std::map<int, cudaGraphExec_t> graphs;  // theta -> instantiated sweep
   std::map<int, int64_t> graph_launches;  // kernels inside each graph
+  cudaGraphExec_t plan_graph = nullptr;   // plan_iteration for plan_opt
+  bool plan_graph_on = true;
+  tafv_options plan_opt{};
+  int64_t plan_graph_launches = 0;
   bool capturing = false;
   int grid_k1 = 0, grid_k2 = 0, grid_k3 = 0;
   int plan_nkeys = 0;
@@ -171,6 +175,7 @@ struct tafv_gpu {
   ~tafv_gpu() {
     cudaSetDevice(device);
     for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    if (plan_graph) cudaGraphExecDestroy(plan_graph);
     void* ptrs[] = {vol, ivol, cen, chl, fcen, adj_off, adj_face, adj_nb, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
                     grad, phi, isub, iwin, tau, cad, raw, tmpa, tmpb, fflag, dtmax, blockmin,
                     cell_counts, face_counts, clist, flist, partials, dplan, stage_buf};
@@ -494,7 +499,6 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys) {
   k_plan_prefix<<<1, 32, 0, h.st>>>(h.dplan);
   ++h.launches;
   CK(cudaGetLastError());
-  CK(cudaEventRecord(h.ev[3], h.st));
   CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
   h.plan_nkeys = nkeys;
 }
@@ -551,12 +555,46 @@ void fill_plan_info(const tafv_gpu& h, tafv_plan_info* out) {
   out->cost_ratio = cost == 0 ? 1.0 : (double)((1ll << h.theta) * (long long)h.N) / (double)cost;
 }
 
+void plan_kernels(tafv_gpu& h, const tafv_options& opt);
+
+// plan_iteration on the device: either the captured plan graph of these
+// options (kernels + the read-back copy, one launch) or direct launches.
 void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
   require(opt.theta_max >= 0, "classify: theta_max must be >= 0");
   require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
   require(h.state_set, "plan: state not set");
   h.has_plan = false;
   CK(cudaEventRecord(h.ev[2], h.st));
+  if (!h.use_graph || !h.plan_graph_on || h.ktime) {
+    plan_kernels(h, opt);
+  } else {
+    const bool same = h.plan_graph && h.plan_opt.theta_max == opt.theta_max &&
+                      h.plan_opt.cfl == opt.cfl && h.plan_opt.dt_cap == opt.dt_cap;
+    if (!same) {
+      if (h.plan_graph) CK(cudaGraphExecDestroy(h.plan_graph));
+      h.plan_graph = nullptr;
+      cudaGraph_t g;
+      const int64_t l0 = h.launches;
+      h.capturing = true;
+      CK(cudaStreamBeginCapture(h.st, cudaStreamCaptureModeThreadLocal));
+      plan_kernels(h, opt);
+      const cudaError_t e = cudaStreamEndCapture(h.st, &g);
+      h.capturing = false;
+      CK(e);
+      CK(cudaGraphInstantiate(&h.plan_graph, g, 0));
+      CK(cudaGraphDestroy(g));
+      h.plan_opt = opt;
+      h.plan_graph_launches = h.launches - l0;
+      h.launches = l0;
+    }
+    CK(cudaGraphLaunch(h.plan_graph, h.st));
+    h.launches += h.plan_graph_launches;
+    h.plan_nkeys = opt.theta_max + 1;
+  }
+  CK(cudaEventRecord(h.ev[3], h.st));
+}
+
+void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
   dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr);
   reset_plan_counts(h);
   k_classify<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.N, h.dtmax, h.dplan, opt.theta_max, h.raw);
@@ -618,6 +656,7 @@ void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options*
     dispatch_dt_max(h, opt->cfl, opt->dt_cap, h.tau);
   }
   enqueue_finish_plan(h, maxl + 1);
+  CK(cudaEventRecord(h.ev[3], h.st));
   CK(cudaStreamSynchronize(h.st));
   accept_plan(h);
   if (!(std::isfinite(h.dt) && h.dt > 0.0)) {  // levels.cpp:54
@@ -1081,6 +1120,8 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     const std::string n = name ? name : "";
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+    } else if (n == "plan_graph") {
+      h->plan_graph_on = value != 0;
     } else if (n == "use_graph") {
       h->use_graph = value != 0;
     } else if (n == "kernel_timing") {
