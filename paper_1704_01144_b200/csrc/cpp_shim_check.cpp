@@ -1,0 +1,85 @@
+// C++ host check of the drop-in boundary: a reference-style caller written
+// against include/tafv_gpu.hpp (the shim over the C ABI). Builds a small
+// config-2-shaped mesh with tafv_mesh_hex, integrates on the GPU, and checks
+// the exception mapping of the reference's error convention
+// (common.hpp:9-19, reference.cpp:93). Prints one line; exit 0 on success.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "tafv_gpu.hpp"
+
+int main() {
+  const int n = 12;
+  std::vector<double> x(n + 1);
+  for (int i = 0; i <= n; ++i) x[i] = double(i) / n;
+  int32_t nc = 0, nf = 0;
+  tafv_mesh_hex(n, n, n, x.data(), x.data(), x.data(), 0.1, 7, 1, &nc, &nf, nullptr, nullptr, nullptr,
+                nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  std::vector<double> vol(nc), cen(3 * nc), chl(nc), fn(3 * nf), fa(nf), fc(3 * nf);
+  std::vector<int32_t> fl(nf), fr(nf), fp(nf);
+  if (tafv_mesh_hex(n, n, n, x.data(), x.data(), x.data(), 0.1, 7, 1, &nc, &nf, vol.data(), cen.data(),
+                    chl.data(), fl.data(), fr.data(), fp.data(), fn.data(), fa.data(), fc.data()) != 0)
+    return 2;
+  const tafv_mesh_view mv{3, nc, nf, vol.data(), cen.data(), chl.data(), fl.data(), fr.data(),
+                          fp.data(), fn.data(), fa.data(), fc.data()};
+  tafv_physics ph{};
+  ph.model = TAFV_EULER;
+  ph.gamma = 1.4;
+  tafv::gpu::Solver s(mv, ph, 0);
+  std::vector<double> w(5 * nc, 0.0);
+  for (int c = 0; c < nc; ++c) {
+    const double dx = cen[3 * c] - 0.5, dy = cen[3 * c + 1] - 0.5, dz = cen[3 * c + 2] - 0.5;
+    const bool in = dx * dx + dy * dy + dz * dz < 0.04;
+    w[5 * c] = in ? 2.0 : 1.0;
+    w[5 * c + 4] = (in ? 10.0 : 1.0) / 0.4;
+  }
+  s.set_state(w.data());
+  tafv::gpu::SolverOptions opt;
+  opt.theta_max = 2;
+  opt.cfl = 0.25;
+  opt.dt_cap = 1e30;
+  const auto recs = tafv::gpu::reference_integrate(s, opt, 4);
+  std::vector<double> W(5 * nc);
+  double t0 = 0;
+  int it = 0;
+  s.get_state(w.data(), W.data(), &t0, &it);
+  bool ok = it == 4 && std::isfinite(t0) && t0 > 0 && recs.size() == 4;
+  for (double v : w) ok = ok && std::isfinite(v);
+  // error convention: invalid_argument for bad options (levels.cpp:20) and a
+  // collapsed stable step (reference.cpp:93); logic_error for an unsmoothed
+  // injected level map.
+  int caught = 0;
+  opt.theta_max = -1;
+  try {
+    tafv::gpu::plan_iteration(s, opt);
+  } catch (const std::invalid_argument&) {
+    ++caught;
+  }
+  opt.theta_max = 2;
+  opt.cfl = 0.0;
+  try {
+    tafv::gpu::plan_iteration(s, opt);
+  } catch (const std::invalid_argument&) {
+    ++caught;
+  }
+  std::vector<int32_t> tau(nc, 0);
+  tau[0] = 3;
+  try {
+    tafv::gpu::inject_levels(s, tau, 1e-3);
+  } catch (const std::logic_error& e) {
+    if (!dynamic_cast<const std::invalid_argument*>(&e)) ++caught;
+  }
+  try {
+    tafv::gpu::run_iteration(s);  // no valid plan after the failures
+  } catch (const std::invalid_argument&) {
+    ++caught;
+  }
+  ok = ok && caught == 4;
+  std::printf("cpp_shim_check %s: %d cells, theta=%d, t=%.6g, levels=%lld/%lld/%lld, caught=%d\n",
+              ok ? "ok" : "FAILED", nc, recs.back().theta, t0, (long long)recs.back().level_cells[0],
+              recs.back().level_cells.size() > 1 ? (long long)recs.back().level_cells[1] : 0LL,
+              recs.back().level_cells.size() > 2 ? (long long)recs.back().level_cells[2] : 0LL, caught);
+  return ok ? 0 : 1;
+}

@@ -52,6 +52,12 @@ struct MeshDev {
   const int* __restrict__ rcf;      // [F] face whose centroid the right side uses (periodic), or null
   const double4* __restrict__ geo;  // [F] {nx, ny, nz, area}
   const double* __restrict__ fcen;  // [F][3]
+  // Hex fast path (DEG 6) per-slot geometry, contiguous per cell so K1's
+  // geometry loads do not wait on the adjacency: {n.x, n.y, n.z, sign*area}
+  // and the limiter's face-centroid offset fc - cc (same IEEE values the
+  // kernel would compute: sign*area is exact, the subtraction is the same).
+  const double4* __restrict__ sgeo;  // [N*6]
+  const double* __restrict__ sdx;    // [N*6][3]
 };
 
 struct StateDev {
@@ -139,8 +145,11 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
 // by slot in CSR order. DEG = 6 is the hex fast path (implicit offsets, fully
 // unrolled slot loop); DEG = 0 reads the CSR offsets. The active count comes
 // from device memory so the launch is graph-capturable.
+#ifndef TAFV_K1_MINB
+#define TAFV_K1_MINB 5  // min resident 128-thread blocks/SM for K1 (register cap 102; measured best)
+#endif
 template <class P, int DEG>
-__global__ void __launch_bounds__(128, 4) k_grad_limit(MeshDev m, StateDev s,
+__global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, StateDev s,
                                                     const int* __restrict__ list,
                                                     const int* __restrict__ n_dev, int front,
                                                     int pred) {
@@ -165,10 +174,17 @@ __global__ void __launch_bounds__(128, 4) k_grad_limit(MeshDev m, StateDev s,
     const int s1 = DEG ? s0 + DEG : m.adj_off[c + 1];
 #pragma unroll
     for (int t = s0; t < s1; ++t) {
-      const int ef = m.adj_face[t], nb = m.adj_nb[t];
-      const int f = slot_face(ef);
-      const double4 gm = m.geo[f];
-      const double scale = slot_sign(ef) * gm.w;
+      const int nb = m.adj_nb[t];
+      double4 gm;
+      double scale;
+      if (DEG == 6 && m.sgeo) {
+        gm = m.sgeo[t];
+        scale = gm.w;
+      } else {
+        const int ef = m.adj_face[t];
+        gm = m.geo[slot_face(ef)];
+        scale = slot_sign(ef) * gm.w;
+      }
       double wf[NV];
       if (nb >= 0) {
         double wn[NV];
@@ -204,9 +220,19 @@ __global__ void __launch_bounds__(128, 4) k_grad_limit(MeshDev m, StateDev s,
       for (int k = 0; k < NV; ++k) alpha[k] = 1.0;
 #pragma unroll
       for (int t = s0; t < s1; ++t) {
-        const int f = slot_face(m.adj_face[t]);
-        const double* fc = m.fcen + 3 * (size_t)f;
-        const double dx0 = fc[0] - cc0, dx1 = fc[1] - cc1, dx2 = fc[2] - cc2;
+        double dx0, dx1, dx2;
+        if (DEG == 6 && m.sdx) {
+          const double* d = m.sdx + 3 * (size_t)t;
+          dx0 = d[0];
+          dx1 = d[1];
+          dx2 = d[2];
+        } else {
+          const int f = slot_face(m.adj_face[t]);
+          const double* fc = m.fcen + 3 * (size_t)f;
+          dx0 = fc[0] - cc0;
+          dx1 = fc[1] - cc1;
+          dx2 = fc[2] - cc2;
+        }
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           double delta = g[k][0] * dx0 + g[k][1] * dx1;
@@ -241,8 +267,11 @@ __device__ __forceinline__ double extrapolate(double w, const double* g, const d
 }
 
 // ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
+#ifndef TAFV_K2_MINB
+#define TAFV_K2_MINB 7
+#endif
 template <class P, bool PRED>
-__global__ void __launch_bounds__(128) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
+__global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
                                                    const int* __restrict__ list,
                                                    const int* __restrict__ n_dev, int front,
                                                    const PlanDev* __restrict__ plan) {

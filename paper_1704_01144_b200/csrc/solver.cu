@@ -109,6 +109,9 @@ struct tafv_gpu {
   int2* lr = nullptr;
   int* rcf = nullptr;
   double4* geo = nullptr;
+  double4* sgeo = nullptr;  // hex fast path per-slot geometry (see MeshDev)
+  double* sdx = nullptr;
+  bool slot_geo = true;
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
@@ -153,7 +156,9 @@ struct tafv_gpu {
   int grid_cap = 148 * 8;
 
   MeshDev mesh_dev() const {
-    return MeshDev{N, F, vol, ivol, cen, chl, adj_off, adj_face, adj_nb, lr, periodic ? rcf : nullptr, geo, fcen};
+    return MeshDev{N,    F,   vol,    ivol,   cen,  chl, adj_off, adj_face, adj_nb, lr,
+                   periodic ? rcf : nullptr, geo, fcen, slot_geo ? sgeo : nullptr,
+                   slot_geo ? sdx : nullptr};
   }
   StateDev state_dev() const { return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin}; }
 
@@ -176,7 +181,7 @@ struct tafv_gpu {
     cudaSetDevice(device);
     for (auto& g : graphs) cudaGraphExecDestroy(g.second);
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
-    void* ptrs[] = {vol, ivol, cen, chl, fcen, adj_off, adj_face, adj_nb, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
+    void* ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, adj_off, adj_face, adj_nb, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
                     grad, phi, isub, iwin, tau, cad, raw, tmpa, tmpb, fflag, dtmax, blockmin,
                     cell_counts, face_counts, clist, flist, partials, dplan, stage_buf};
     for (void* p : ptrs)
@@ -328,6 +333,21 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   up(h.ivol, ivol);
   h.deg6 = true;
   for (int i = 0; i <= N && h.deg6; ++i) h.deg6 = off[i] == 6 * i;
+  if (h.deg6) {
+    std::vector<double4> sgeo(h.M);
+    std::vector<double> sdx(3 * (size_t)h.M);
+    for (int i = 0; i < N; ++i)
+      for (int t = 6 * i; t < 6 * i + 6; ++t) {
+        const int j = adj_face[t] >= 0 ? adj_face[t] : ~adj_face[t];
+        const double4 g = geo[j];
+        sgeo[t] = make_double4(g.x, g.y, g.z, sgn[t] * g.w);
+        for (int d = 0; d < 3; ++d) sdx[3 * (size_t)t + d] = fcen[3 * (size_t)j + d] - cen[3 * (size_t)i + d];
+      }
+    h.sgeo = dalloc<double4>(h.M);
+    up(h.sgeo, sgeo);
+    h.sdx = dalloc<double>(3 * (size_t)h.M);
+    up(h.sdx, sdx);
+  }
   h.cen = dalloc<double>(3 * (size_t)N);
   up(h.cen, cen);
   h.chl = dalloc<double>(N);
@@ -1120,6 +1140,10 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     const std::string n = name ? name : "";
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+    } else if (n == "slot_geo") {
+      h->slot_geo = value != 0;
+      for (auto& g : h->graphs) cudaGraphExecDestroy(g.second);
+      h->graphs.clear();
     } else if (n == "plan_graph") {
       h->plan_graph_on = value != 0;
     } else if (n == "use_graph") {

@@ -196,8 +196,8 @@ def test_divergence_detected(gpu):
         s.reference_integrate(cfg.options(), 3)
 
 
-@pytest.mark.parametrize("use_graph", [0, 1])
-def test_graph_and_direct_launch_bitwise(use_graph, gpu):
+@pytest.mark.parametrize("use_graph,slot_geo", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, gpu):
     """The CUDA-graph sweep and the direct-launch sweep both reproduce the
     oracle bitwise (records included), through reference_integrate."""
     from oracle import OracleSolver
@@ -207,6 +207,7 @@ def test_graph_and_direct_launch_bitwise(use_graph, gpu):
     opt = cfg.options()
     g = Solver(mesh, "euler")
     g.set_flag("use_graph", use_graph)
+    g.set_flag("slot_geo", slot_geo)
     g.set_state(w0)
     rg = g.reference_integrate(opt, 6)
     o = OracleSolver(mesh, "euler", threads=8)
@@ -221,3 +222,13 @@ def test_graph_and_direct_launch_bitwise(use_graph, gpu):
     assert [r["level_cells"] for r in rg] == [r["level_cells"] for r in ro]
     assert [r["iteration"] for r in rg] == [r["iteration"] for r in ro]
     assert [r["t_start"] for r in rg] == [r["t_start"] for r in ro]
+
+
+def test_cpp_shim_caller(gpu):
+    """A reference-style C++ caller (include/tafv_gpu.hpp) integrates on the
+    GPU and sees the reference's exception classes."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "..", "paper_1704_01144_b200", "tafv_cpp_check")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "cpp_shim_check ok" in r.stdout
