@@ -191,6 +191,25 @@ int tafv_gpu_kernel_times(tafv_gpu* h, double* ms6, int64_t* counts6, int64_t* i
 /* n_cells, n_faces, adjacency slots, nv of the uploaded mesh/physics. */
 int tafv_gpu_mesh_info(tafv_gpu* h, int64_t* info4);
 
+/* ---- multi-GPU decomposition (host only) -----------------
+ * Contiguous slab partition along `axis` balancing `weight` (NULL = cell
+ * count; level cost 2^(theta-tau) as DistDriver::repartition weighs,
+ * exchange.cpp:598-603). */
+int tafv_partition_slabs(const tafv_mesh_view* mesh, int32_t nranks, int32_t axis,
+                         const double* weight, int32_t* rank_of_cell);
+
+/* The shard of `rank`: owned cells + 2-ring halo, faces touching owned or
+ * ring-1 cells, and per-peer exchange lists (the reference's ghost
+ * components, ce.cpp:66-90, widened to two rings). counts[8] = n_own, n_r1,
+ * n_r2, n_faces, n_faces_touching_owned, n_peers, send total, recv total;
+ * cells/faces = local -> global ids (ascending); send/recv lists are local
+ * cell ids, peer by peer, ascending global id. Any output may be NULL. */
+int tafv_shard_describe(const tafv_mesh_view* mesh, const int32_t* rank_of_cell, int32_t rank,
+                        int32_t nranks, int32_t* counts, int32_t* cells, int32_t* faces,
+                        int32_t* peers, int32_t* send_counts, int32_t* recv_counts,
+                        int32_t* send_flat, int32_t* recv_flat);
+const char* tafv_shard_last_error(void);
+
 /* 3D hexahedral mesh generator (new: the reference generator is 1D/2D only,
  * mesh.cpp:302-317). Tensor-product node lattice x[nx+1], y[ny+1], z[nz+1],
  * interior nodes jittered uniformly by +-jitter of the local spacing

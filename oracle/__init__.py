@@ -319,7 +319,7 @@ class RefSolver(_SolverBase):
 
 
 class OracleMesh:
-    def __init__(self, mesh):
+    def __init__(self, mesh, closure_mask=None):
         self.lib = oracle_lib()
         self.mesh = mesh
         self.nc = int(len(mesh["vol"]))
@@ -329,8 +329,12 @@ class OracleMesh:
                 _f64(mesh["fc"])]
         self._keep = arrs
         h = C.c_void_p()
-        rc = self.lib.orc_mesh_create(int(mesh["dim"]), self.nc, self.nf,
-                                      *[a.ctypes.data_as(C.c_void_p) for a in arrs], C.byref(h))
+        mask = None if closure_mask is None else np.ascontiguousarray(closure_mask, dtype=np.uint8)
+        self._mask = mask
+        rc = self.lib.orc_mesh_create_masked(int(mesh["dim"]), self.nc, self.nf,
+                                             *[a.ctypes.data_as(C.c_void_p) for a in arrs],
+                                             mask.ctypes.data_as(C.c_void_p) if mask is not None else None,
+                                             C.byref(h))
         _check(self.lib, rc, "orc_last_error")
         self.h = h
 

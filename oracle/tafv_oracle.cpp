@@ -185,9 +185,11 @@ void build_adjacency(Mesh& m) {
   }
 }
 
-// mesh.cpp:273-284 (plus the z component in 3D).
-void check_closure(const Mesh& m) {
+// mesh.cpp:273-284 (plus the z component in 3D). `mask` (optional) limits
+// the check to cells with a complete face set (a shard's ring-2 cells are not).
+void check_closure(const Mesh& m, const uint8_t* mask = nullptr) {
   for (int c = 0; c < m.nc; ++c) {
+    if (mask && !mask[c]) continue;
     double sx = 0.0, sy = 0.0, sz = 0.0;
     for (int t = m.adj_off[c]; t < m.adj_off[c + 1]; ++t) {
       const int f = m.adj_face[t];
@@ -1055,9 +1057,21 @@ const char* orc_last_error() { return g_err.c_str(); }
 
 // Mesh from reference-layout arrays (Face/Cell of mesh.hpp:26-39, Vec3).
 // Builds the ascending-face-id CSR adjacency and checks closure.
+int orc_mesh_create_masked(int dim, int nc, int nf, const double* vol, const double* cen,
+                           const double* chl, const int* fl, const int* fr, const int* fp,
+                           const double* fn, const double* fa, const double* fc,
+                           const uint8_t* closure_mask, void** out);
+
 int orc_mesh_create(int dim, int nc, int nf, const double* vol, const double* cen,
                     const double* chl, const int* fl, const int* fr, const int* fp,
                     const double* fn, const double* fa, const double* fc, void** out) {
+  return orc_mesh_create_masked(dim, nc, nf, vol, cen, chl, fl, fr, fp, fn, fa, fc, nullptr, out);
+}
+
+int orc_mesh_create_masked(int dim, int nc, int nf, const double* vol, const double* cen,
+                           const double* chl, const int* fl, const int* fr, const int* fp,
+                           const double* fn, const double* fa, const double* fc,
+                           const uint8_t* closure_mask, void** out) {
   return guard([&] {
     require(nc >= 0 && nf >= 0, "mesh: negative counts");
     auto m = std::make_unique<Mesh>();
@@ -1074,7 +1088,7 @@ int orc_mesh_create(int dim, int nc, int nf, const double* vol, const double* ce
     m->fa.assign(fa, fa + nf);
     m->fc.assign(fc, fc + 3 * size_t(nf));
     build_adjacency(*m);
-    check_closure(*m);
+    check_closure(*m, closure_mask);
     *out = m.release();
   });
 }

@@ -105,6 +105,7 @@ EXPORTS = [
     "tafv_gpu_get_state", "tafv_gpu_plan", "tafv_gpu_inject_levels", "tafv_gpu_get_plan_lists",
     "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_get_array",
     "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex",
+    "tafv_partition_slabs", "tafv_shard_describe", "tafv_shard_last_error",
 ]
 
 _lib = None
@@ -138,5 +139,8 @@ def lib():
     L.tafv_gpu_mesh_info.argtypes = [vp, vp]
     L.tafv_mesh_hex.argtypes = [i32, i32, i32, vp, vp, vp, dbl, C.c_uint64, i32,
                                 C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    L.tafv_partition_slabs.argtypes = [C.POINTER(MeshView), i32, i32, vp, vp]
+    L.tafv_shard_describe.argtypes = [C.POINTER(MeshView), vp, i32, i32] + [vp] * 8
+    L.tafv_shard_last_error.restype = C.c_char_p
     _lib = L
     return L

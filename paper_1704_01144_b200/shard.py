@@ -1,0 +1,86 @@
+"""Python view of the multi-GPU decomposition (C ABI in include/tafv_gpu.h:
+tafv_partition_slabs, tafv_shard_describe; host code, no GPU needed)."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def mesh_view(mesh):
+    keep = {k: np.ascontiguousarray(mesh[k], dtype=np.float64 if k in ("vol", "cen", "chl", "fn", "fa", "fc")
+                                    else np.int32) for k in ("vol", "cen", "chl", "fl", "fr", "fp", "fn", "fa", "fc")}
+    mv = N.MeshView(int(mesh["dim"]), len(keep["vol"]), len(keep["fa"]),
+                    *[_ptr(keep[k]) for k in ("vol", "cen", "chl", "fl", "fr", "fp", "fn", "fa", "fc")])
+    return mv, keep
+
+
+def partition_slabs(mesh, nranks, axis=0, weight=None):
+    lib = N.lib()
+    mv, keep = mesh_view(mesh)
+    out = np.empty(len(mesh["vol"]), dtype=np.int32)
+    w = None if weight is None else np.ascontiguousarray(weight, dtype=np.float64)
+    if lib.tafv_partition_slabs(C.byref(mv), nranks, axis, _ptr(w), _ptr(out)) != 0:
+        raise ValueError(lib.tafv_shard_last_error().decode())
+    return out
+
+
+def describe(mesh, rank_of_cell, rank, nranks):
+    """Local cells (global ids, with ring class), faces and exchange lists."""
+    lib = N.lib()
+    mv, keep = mesh_view(mesh)
+    roc = np.ascontiguousarray(rank_of_cell, dtype=np.int32)
+    cnt = np.zeros(8, dtype=np.int32)
+    rc = lib.tafv_shard_describe(C.byref(mv), _ptr(roc), rank, nranks, _ptr(cnt), *([None] * 7))
+    if rc != 0:
+        raise ValueError(lib.tafv_shard_last_error().decode())
+    n_own, n_r1, n_r2, nf, nfo, npeer, st, rt = (int(x) for x in cnt)
+    cells = np.empty(n_own + n_r1 + n_r2, dtype=np.int32)
+    faces = np.empty(nf, dtype=np.int32)
+    peers = np.empty(max(1, npeer), dtype=np.int32)
+    sc = np.empty(max(1, npeer), dtype=np.int32)
+    rcn = np.empty(max(1, npeer), dtype=np.int32)
+    sf = np.empty(max(1, st), dtype=np.int32)
+    rf = np.empty(max(1, rt), dtype=np.int32)
+    lib.tafv_shard_describe(C.byref(mv), _ptr(roc), rank, nranks, None, _ptr(cells), _ptr(faces),
+                            _ptr(peers), _ptr(sc), _ptr(rcn), _ptr(sf), _ptr(rf))
+    send, recv, so, ro = {}, {}, 0, 0
+    for i in range(npeer):
+        send[int(peers[i])] = sf[so:so + sc[i]].copy()
+        recv[int(peers[i])] = rf[ro:ro + rcn[i]].copy()
+        so += int(sc[i])
+        ro += int(rcn[i])
+    # ring class per local cell: 0 owned, 1 face neighbour of an owned cell, 2 other
+    owned = roc[cells] == rank
+    g2l = np.full(len(roc), -1, dtype=np.int64)
+    g2l[cells] = np.arange(len(cells))
+    fl, fr = g2l[mesh["fl"][faces]], mesh["fr"][faces]
+    fr = np.where(fr >= 0, g2l[np.maximum(fr, 0)], -1)
+    cls = np.where(owned, 0, 2).astype(np.int8)
+    inner = fr >= 0
+    a, b = fl[inner], fr[inner]
+    cls[b[owned[a] & ~owned[b]]] = 1
+    cls[a[owned[b] & ~owned[a]]] = 1
+    assert (cls == 0).sum() == n_own and (cls == 1).sum() == n_r1 and (cls == 2).sum() == n_r2
+    return {"cells": cells, "faces": faces, "n_own": n_own, "n_r1": n_r1, "n_r2": n_r2,
+            "n_faces_touch_own": nfo, "send": send, "recv": recv, "cls": cls}
+
+
+def local_mesh(mesh, sh):
+    """Reference-layout mesh dict of a shard (local ids = ascending global)."""
+    cells, faces = sh["cells"], sh["faces"]
+    g2l = np.full(len(mesh["vol"]), -1, dtype=np.int32)
+    g2l[cells] = np.arange(len(cells), dtype=np.int32)
+    fr = mesh["fr"][faces]
+    return {
+        "dim": mesh["dim"], "vol": mesh["vol"][cells], "cen": mesh["cen"][cells], "chl": mesh["chl"][cells],
+        "fl": g2l[mesh["fl"][faces]], "fr": np.where(fr >= 0, g2l[np.maximum(fr, 0)], -1).astype(np.int32),
+        "fp": np.full(len(faces), -1, dtype=np.int32), "fn": mesh["fn"][faces], "fa": mesh["fa"][faces],
+        "fc": mesh["fc"][faces],
+    }
