@@ -210,6 +210,28 @@ int tafv_shard_describe(const tafv_mesh_view* mesh, const int32_t* rank_of_cell,
                         int32_t* send_flat, int32_t* recv_flat);
 const char* tafv_shard_last_error(void);
 
+/* ---- multi-GPU ranks -------------------------------------------------------
+ * A communicator replaces the reference's Transport + RankComm
+ * (transport.hpp, exchange.cpp:126-322): NCCL (one process per GPU; get the
+ * 128-byte unique id on rank 0 and broadcast it) or an in-process loopback
+ * for `nranks` host threads (one handle each, possibly on one GPU). */
+typedef struct tafv_comm tafv_comm;
+int tafv_comm_nccl_unique_id(uint8_t* out128);
+int tafv_comm_create_nccl(const uint8_t* id128, int32_t rank, int32_t nranks, int device,
+                          tafv_comm** out);
+int tafv_comm_create_loopback(int32_t nranks, tafv_comm** out);
+void tafv_comm_destroy(tafv_comm* comm);
+
+/* One rank of a decomposed run (DistDriver, exchange.cpp:541-660): the
+ * GLOBAL mesh and partition in, the rank's shard (owned cells + 2-ring halo)
+ * resident on `device`. Afterwards every call is collective over the
+ * communicator's ranks; set_state / inject_levels take GLOBAL arrays,
+ * get_state writes the rank's OWNED rows into the global arrays, records are
+ * global. Periodic meshes are not supported in this mode. */
+int tafv_gpu_create_shard(const tafv_mesh_view* global_mesh, const tafv_physics* physics, int device,
+                          const int32_t* rank_of_cell, int32_t rank, tafv_comm* comm,
+                          tafv_gpu** out);
+
 /* 3D hexahedral mesh generator (new: the reference generator is 1D/2D only,
  * mesh.cpp:302-317). Tensor-product node lattice x[nx+1], y[ny+1], z[nz+1],
  * interior nodes jittered uniformly by +-jitter of the local spacing

@@ -106,6 +106,8 @@ EXPORTS = [
     "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_get_array",
     "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex",
     "tafv_partition_slabs", "tafv_shard_describe", "tafv_shard_last_error",
+    "tafv_comm_nccl_unique_id", "tafv_comm_create_nccl", "tafv_comm_create_loopback",
+    "tafv_comm_destroy", "tafv_gpu_create_shard",
 ]
 
 _lib = None
@@ -142,5 +144,12 @@ def lib():
     L.tafv_partition_slabs.argtypes = [C.POINTER(MeshView), i32, i32, vp, vp]
     L.tafv_shard_describe.argtypes = [C.POINTER(MeshView), vp, i32, i32] + [vp] * 8
     L.tafv_shard_last_error.restype = C.c_char_p
+    L.tafv_comm_nccl_unique_id.argtypes = [vp]
+    L.tafv_comm_create_nccl.argtypes = [vp, i32, i32, C.c_int, C.POINTER(vp)]
+    L.tafv_comm_create_loopback.argtypes = [i32, C.POINTER(vp)]
+    L.tafv_comm_destroy.argtypes = [vp]
+    L.tafv_comm_destroy.restype = None
+    L.tafv_gpu_create_shard.argtypes = [C.POINTER(MeshView), C.POINTER(Physics), C.c_int, vp, i32, vp,
+                                        C.POINTER(vp)]
     _lib = L
     return L

@@ -81,6 +81,44 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p) if a is not None else None
 
 
+class Comm:
+    """Communicator of a decomposed run (tafv_comm): NCCL across processes or
+    an in-process loopback for ranks run as threads."""
+
+    def __init__(self, h):
+        self.lib = N.lib()
+        self.h = h
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = (C.c_uint8 * 128)()
+        if N.lib().tafv_comm_nccl_unique_id(buf) != 0:
+            raise CudaError("ncclGetUniqueId failed")
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, unique_id, rank, nranks, device=0):
+        lib = N.lib()
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        rc = lib.tafv_comm_create_nccl(buf, rank, nranks, device, C.byref(h))
+        if rc != 0:
+            raise _EXC.get(rc, TafvError)(lib.tafv_gpu_last_error(None).decode())
+        return cls(h)
+
+    @classmethod
+    def loopback(cls, nranks):
+        h = C.c_void_p()
+        if N.lib().tafv_comm_create_loopback(nranks, C.byref(h)) != 0:
+            raise InvalidArgument("loopback: nranks must be >= 1")
+        return cls(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tafv_comm_destroy(self.h)
+            self.h = None
+
+
 class Solver:
     """One mesh + SolverState resident on one GPU (a ``tafv_gpu`` handle).
 
@@ -88,7 +126,9 @@ class Solver:
     ``dim, vol, cen, chl, fl, fr, fp, fn, fa, fc``.
     """
 
-    def __init__(self, mesh, model="euler", a=(1.0, 0.0), gamma=1.4, device=0):
+    def __init__(self, mesh, model="euler", a=(1.0, 0.0), gamma=1.4, device=0, shard=None):
+        """shard=(rank_of_cell, rank, comm): one rank of a decomposed run
+        over the GLOBAL mesh (tafv_gpu_create_shard)."""
         self.lib = N.lib()
         self.model = model
         self.nv = 5 if model == "euler" else 1
@@ -106,7 +146,15 @@ class Solver:
             "face_partner", "face_normal", "face_area", "face_centroid")])
         ph = N.Physics(MODELS[model], (C.c_double * 3)(a[0], a[1], a[2] if len(a) > 2 else 0.0), gamma)
         h = C.c_void_p()
-        rc = self.lib.tafv_gpu_create(C.byref(mv), C.byref(ph), device, C.byref(h))
+        if shard is None:
+            rc = self.lib.tafv_gpu_create(C.byref(mv), C.byref(ph), device, C.byref(h))
+        else:
+            roc, rank, comm = shard
+            self._roc = np.ascontiguousarray(roc, dtype=np.int32)
+            rc = self.lib.tafv_gpu_create_shard(C.byref(mv), C.byref(ph), device, _ptr(self._roc), int(rank),
+                                                comm.h, C.byref(h))
+            self.rank = int(rank)
+            self.owned = self._roc == self.rank
         if rc != 0:
             raise _EXC.get(rc, TafvError)(self.lib.tafv_gpu_last_error(None).decode())
         self.h = h
@@ -137,8 +185,9 @@ class Solver:
         self._c(self.lib.tafv_gpu_set_state(self.h, _ptr(w), _ptr(Wa), float(t0), int(iteration)))
 
     def get_state(self):
-        w = np.empty((self.nc, self.nv))
-        W = np.empty((self.nc, self.nv))
+        """(w, W, t0, iteration); a shard fills only its owned rows (zeros elsewhere)."""
+        w = np.zeros((self.nc, self.nv))
+        W = np.zeros((self.nc, self.nv))
         t0, it = C.c_double(), C.c_int32()
         self._c(self.lib.tafv_gpu_get_state(self.h, _ptr(w), _ptr(W), C.byref(t0), C.byref(it)))
         if self.nv == 1:

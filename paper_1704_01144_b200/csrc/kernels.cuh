@@ -80,8 +80,11 @@ struct PlanDev {
   long long face_count[kMaxLevels];
   long long fringe_count[kMaxLevels];
   double totals[8];     // sum of W per component after the last iteration
-  int ncell_prefix[kMaxLevels];  // |{c : tau_c <= l}|: active cells of subiteration level l
-  int nface_prefix[kMaxLevels];  // |{f : cadence_f <= l}|
+  int ncell_prefix[kMaxLevels];  // |{c owned : tau_c <= l}|: K3 active cells of level l
+  int nface_prefix[kMaxLevels];  // |{f touching owned : cadence_f <= l}|: K2 active faces
+  int nk1_prefix[kMaxLevels];    // |{c owned or ring 1 : tau_c <= l}|: K1 active cells
+  long long k1_count[kMaxLevels];    // per-level counts of the K1 list (owned + ring 1)
+  long long gcell_count[kMaxLevels]; // owned counts summed over ranks (records, theta)
 };
 
 // ---- staging: pure function of the committed/predicted state ---------------
@@ -461,11 +464,11 @@ __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks,
 template <class P>
 __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParams pp, double cfl,
                                                 double dt_cap, double* dt_max, double* block_min,
-                                                const int8_t* tau_scale) {
+                                                const int8_t* tau_scale, int n) {
   constexpr int NV = P::NV;
   double lowest = __longlong_as_double(0x7ff0000000000000ll);
   const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n_cells; c += stride) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     double w[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) w[k] = s.w[(size_t)c * NV + k];
@@ -520,9 +523,9 @@ __global__ void k_classify(int n, const double* dt_max, const PlanDev* plan, int
 }
 
 // levels.cpp:33-46 one Jacobi sweep: out = min(in, 1 + min over neighbours).
-__global__ void k_smooth(MeshDev m, const int8_t* in, int8_t* out) {
+__global__ void k_smooth(MeshDev m, const int8_t* in, int8_t* out, int n) {
   const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < m.n_cells; c += stride) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     int bound = in[c];
     const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
     for (int t = s0; t < s1; ++t) {
@@ -662,15 +665,42 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(const int8_t* 
 
 // Active-set sizes of every subiteration level (prefix sums of the per-level
 // counts) for the graph-captured sweep, which reads its counts on device.
-__global__ void k_plan_prefix(PlanDev* plan) {
+// alias_k1: single-domain run, the K1 list is the K3 list.
+__global__ void k_plan_prefix(PlanDev* plan, int alias_k1) {
   if (threadIdx.x != 0) return;
-  long long c = 0, f = 0;
+  long long c = 0, f = 0, k = 0;
   for (int l = 0; l < kMaxLevels; ++l) {
+    if (alias_k1) plan->k1_count[l] = plan->cell_count[l];
     c += plan->cell_count[l];
     f += plan->face_count[l];
+    k += plan->k1_count[l];
     plan->ncell_prefix[l] = (int)c;
     plan->nface_prefix[l] = (int)f;
+    plan->nk1_prefix[l] = (int)k;
+    plan->gcell_count[l] = plan->cell_count[l];
   }
+}
+
+// Halo rows: pack owned rows for the peers, unpack received halo rows.
+__global__ void k_pack_rows(const double* src, const int* idx, int n, int width, double* dst) {
+  const size_t total = (size_t)n * width;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    dst[i] = src[(size_t)idx[i / width] * width + i % width];
+}
+__global__ void k_unpack_rows(const double* src, const int* idx, int n, int width, double* dst) {
+  const size_t total = (size_t)n * width;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    dst[(size_t)idx[i / width] * width + i % width] = src[i];
+}
+__global__ void k_pack_i8(const int8_t* src, const int* idx, int n, int8_t* dst) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[idx[i]];
+}
+__global__ void k_unpack_i8(const int8_t* src, const int* idx, int n, int8_t* dst) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[idx[i]] = src[i];
 }
 
 // ---- state movement (original <-> internal numbering) -----------------------

@@ -16,9 +16,12 @@
 // to size the 2^theta sweep); everything else stays on the device.
 
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -27,7 +30,9 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "kernels.cuh"
+#include "shard.h"
 #include "tafv_gpu.h"
 
 using namespace tafv;
@@ -150,6 +155,25 @@ struct tafv_gpu {
   int64_t kcnt[kNumKinds] = {};
   int64_t kitems[kNumKinds][3] = {};  // active cells, active faces, fringe cells per kind
 
+  // multi-GPU shard. Internal cells [0, n_own) are owned,
+  // [n_own, n_k1) ring 1, [n_k1, N) ring 2; faces [0, F_own) touch an owned
+  // cell. Single domain: n_own = n_k1 = N, F_own = F, no comm.
+  int rank = 0, nranks = 1, n_own = 0, n_k1 = 0, F_own = 0, N_global = 0;
+  tafv_comm* comm = nullptr;
+  std::vector<int> shard_cells;  // local original id -> global cell id
+  struct Peer {
+    int rank, nsend, nrecv, soff, roff;
+  };
+  std::vector<Peer> peers;
+  int *d_send_idx = nullptr, *d_recv_idx = nullptr;
+  int send_total = 0, recv_total = 0;
+  double *sendbuf = nullptr, *recvbuf = nullptr;
+  int* klist = nullptr;       // K1 list (owned + ring 1); == clist when single domain
+  int* k1_counts = nullptr;
+  int ntile_k = 0;
+  long long gcount[kMaxLevels] = {};  // owned counts over all ranks
+  bool sharded() const { return comm != nullptr; }
+
   // stats
   int64_t launches = 0;
   double ms[3] = {0, 0, 0};
@@ -181,9 +205,12 @@ struct tafv_gpu {
     cudaSetDevice(device);
     for (auto& g : graphs) cudaGraphExecDestroy(g.second);
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
-    void* ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, adj_off, adj_face, adj_nb, lr, rcf, geo, d_cperm, d_fperm, w, W, wp,
-                    grad, phi, isub, iwin, tau, cad, raw, tmpa, tmpb, fflag, dtmax, blockmin,
-                    cell_counts, face_counts, clist, flist, partials, dplan, stage_buf};
+    void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
+                    adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
+                    grad, phi,   isub,     iwin,     tau,    cad,    raw,      tmpa,    tmpb,
+                    fflag, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
+                    stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
+                    klist != clist ? klist : nullptr, k1_counts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
@@ -194,10 +221,141 @@ struct tafv_gpu {
   }
 };
 
+
+// ---- transports (comm.h) ------------------------------------------------------
+namespace {
+
+#define NK(x)                                                                        \
+  do {                                                                               \
+    const ncclResult_t r_ = (x);                                                     \
+    if (r_ != ncclSuccess) throw Error{TAFV_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+struct NcclComm final : tafv_comm {
+  ncclComm_t c = nullptr;
+  NcclComm(const void* id, int rank, int n) {
+    rank_count = n;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof uid);
+    NK(ncclCommInitRank(&c, n, uid, rank));
+  }
+  ~NcclComm() override {
+    if (c) ncclCommDestroy(c);
+  }
+  bool capturable() const override { return true; }
+  void allreduce_min_f64(int, double* d, int n, cudaStream_t st) override {
+    NK(ncclAllReduce(d, d, n, ncclFloat64, ncclMin, c, st));
+  }
+  void allreduce_max_i32(int, int* d, int n, cudaStream_t st) override {
+    NK(ncclAllReduce(d, d, n, ncclInt32, ncclMax, c, st));
+  }
+  void allreduce_sum_f64(int, double* d, int n, cudaStream_t st) override {
+    NK(ncclAllReduce(d, d, n, ncclFloat64, ncclSum, c, st));
+  }
+  void allreduce_sum_i64(int, long long* d, int n, cudaStream_t st) override {
+    NK(ncclAllReduce(d, d, n, ncclInt64, ncclSum, c, st));
+  }
+  void exchange(tafv_gpu& h, int bpr) override {
+    // grouped send/recv with every peer (the slab neighbours), one launch
+    NK(ncclGroupStart());
+    for (const auto& p : h.peers) {
+      char* sb = reinterpret_cast<char*>(h.sendbuf) + (size_t)p.soff * bpr;
+      char* rb = reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr;
+      if (p.nsend) NK(ncclSend(sb, (size_t)p.nsend * bpr, ncclChar, p.rank, c, h.st));
+      if (p.nrecv) NK(ncclRecv(rb, (size_t)p.nrecv * bpr, ncclChar, p.rank, c, h.st));
+    }
+    NK(ncclGroupEnd());
+  }
+};
+
+// R in-process ranks (host threads, one stream each). Host barriers order
+// the ranks; data moves by device copies on the receiver's stream after the
+// producers' streams were synchronised. No device-side waiting.
+struct LoopbackComm final : tafv_comm {
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<tafv_gpu*> members;
+  std::vector<std::vector<double>> f64;
+  std::vector<std::vector<long long>> i64;
+  std::vector<std::vector<int>> i32;
+  explicit LoopbackComm(int n) : members(n, nullptr), f64(n), i64(n), i32(n) { rank_count = n; }
+  bool capturable() const override { return false; }
+  void attach(int rank, tafv_gpu* h) override { members[rank] = h; }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == rank_count) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+  template <class T, class Op>
+  void allreduce(std::vector<std::vector<T>>& slots, int rank, T* d, int n, cudaStream_t st, Op op) {
+    slots[rank].resize(n);
+    CK(cudaMemcpyAsync(slots[rank].data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    barrier();
+    std::vector<T> r = slots[0];
+    for (int q = 1; q < rank_count; ++q)
+      for (int i = 0; i < n; ++i) r[i] = op(r[i], slots[q][i]);
+    CK(cudaMemcpyAsync(d, r.data(), n * sizeof(T), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    barrier();
+  }
+  void allreduce_min_f64(int rank, double* d, int n, cudaStream_t st) override {
+    allreduce(f64, rank, d, n, st, [](double a, double b) { return (b < a) ? b : a; });
+  }
+  void allreduce_max_i32(int rank, int* d, int n, cudaStream_t st) override {
+    allreduce(i32, rank, d, n, st, [](int a, int b) { return a < b ? b : a; });
+  }
+  void allreduce_sum_f64(int rank, double* d, int n, cudaStream_t st) override {
+    allreduce(f64, rank, d, n, st, [](double a, double b) { return a + b; });
+  }
+  void allreduce_sum_i64(int rank, long long* d, int n, cudaStream_t st) override {
+    allreduce(i64, rank, d, n, st, [](long long a, long long b) { return a + b; });
+  }
+  void exchange(tafv_gpu& h, int bpr) override {
+    CK(cudaStreamSynchronize(h.st));  // my packed rows are in sendbuf
+    barrier();
+    for (const auto& p : h.peers) {
+      const tafv_gpu& g = *members[p.rank];
+      const tafv_gpu::Peer* back = nullptr;
+      for (const auto& q : g.peers)
+        if (q.rank == h.rank) back = &q;
+      if (!back || back->nsend != p.nrecv) throw Error{TAFV_ELOGIC, "loopback: mismatched exchange lists"};
+      if (p.nrecv)
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr,
+                           reinterpret_cast<const char*>(g.sendbuf) + (size_t)back->soff * bpr,
+                           (size_t)p.nrecv * bpr, cudaMemcpyDeviceToDevice, h.st));
+    }
+    CK(cudaStreamSynchronize(h.st));  // peers may reuse their send buffers
+    barrier();
+  }
+};
+
+}  // namespace
+
+tafv_comm* make_loopback_comm(int nranks) { return new LoopbackComm(nranks); }
+tafv_comm* make_nccl_comm(const void* id, int rank, int nranks) { return new NcclComm(id, rank, nranks); }
+int nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TAFV_ENCCL;
+  std::memcpy(out, &id, sizeof id);
+  return TAFV_OK;
+}
+
 namespace {
 
 // ---- mesh upload -----------------------------------------------------------
-void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
+// cls (optional): per original cell 0 owned / 1 ring 1 / 2 ring 2 (shards);
+// touch (optional): per original face 1 if it has an owned side.
+void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
+                 const uint8_t* touch = nullptr) {
   const int N = mv.n_cells, F = mv.n_faces;
   require(N > 0 && F >= 0, "mesh: empty mesh");
   require(mv.dim >= 1 && mv.dim <= 3, "mesh: dim must be 1, 2 or 3");
@@ -218,7 +376,8 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
       lo[d] = std::min(lo[d], mv.cell_centroid[3 * (size_t)c + d]);
       hi[d] = std::max(hi[d], mv.cell_centroid[3 * (size_t)c + d]);
     }
-  std::vector<std::pair<uint64_t, int>> key(N);
+  // (ring class, Morton, id): owned cells first, then ring 1, then ring 2.
+  std::vector<std::pair<std::pair<int, uint64_t>, int>> key(N);
   for (int c = 0; c < N; ++c) {
     uint64_t k = 0;
     for (int d = 0; d < 3; ++d) {
@@ -227,9 +386,15 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
       const uint64_t q = (uint64_t)std::min(2097151.0, std::max(0.0, u * 2097151.0));
       k |= spread3(q) << d;
     }
-    key[c] = {k, c};
+    key[c] = {{cls ? (int)cls[c] : 0, k}, c};
   }
   std::sort(key.begin(), key.end());
+  h.n_own = h.n_k1 = 0;
+  for (int c = 0; c < N; ++c) {
+    const int k = cls ? cls[c] : 0;
+    if (k == 0) ++h.n_own;
+    if (k <= 1) ++h.n_k1;
+  }
   h.cperm.resize(N);
   std::vector<int> cinv(N);
   for (int i = 0; i < N; ++i) {
@@ -239,16 +404,20 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   key.clear();
   key.shrink_to_fit();
 
-  // Face order: grouped by internal left cell, stable in original face id.
-  std::vector<int> fstart(N + 1, 0);
-  for (int f = 0; f < F; ++f) ++fstart[cinv[mv.face_left[f]] + 1];
-  for (int i = 0; i < N; ++i) fstart[i + 1] += fstart[i];
+  // Face order: faces touching an owned cell first; within each group by
+  // internal left cell, stable in original face id.
+  h.F_own = 0;
+  for (int f = 0; f < F; ++f) h.F_own += touch ? (touch[f] ? 1 : 0) : 1;
+  std::vector<int> fstart(2 * (size_t)N + 1, 0);
+  auto fkey = [&](int f) { return (touch && !touch[f] ? N : 0) + cinv[mv.face_left[f]]; };
+  for (int f = 0; f < F; ++f) ++fstart[fkey(f) + 1];
+  for (int i = 0; i < 2 * N; ++i) fstart[i + 1] += fstart[i];
   h.fperm.resize(F);
   std::vector<int> finv(F);
   {
     std::vector<int> cur(fstart.begin(), fstart.end() - 1);
     for (int f = 0; f < F; ++f) {
-      const int j = cur[cinv[mv.face_left[f]]]++;
+      const int j = cur[fkey(f)]++;
       h.fperm[j] = f;
       finv[f] = j;
     }
@@ -287,8 +456,9 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
       }
     }
   }
-  // Geometric closure (mesh.cpp:273-284), same slot order and expressions.
-  for (int i = 0; i < N; ++i) {
+  // Geometric closure (mesh.cpp:273-284), same slot order and expressions,
+  // on every cell with a complete face set (a shard's ring 2 has not).
+  for (int i = 0; i < h.n_k1; ++i) {
     double s[3] = {0.0, 0.0, 0.0};
     for (int t = off[i]; t < off[i + 1]; ++t) {
       const int j = adj_face[t] >= 0 ? adj_face[t] : ~adj_face[t];
@@ -331,12 +501,14 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv) {
   for (int i = 0; i < N; ++i) ivol[i] = 1.0 / vol[i];  // same IEEE quotient as the device's
   h.ivol = dalloc<double>(N);
   up(h.ivol, ivol);
+  // Hex fast path: every cell the hot kernels visit (owned + ring 1, which
+  // lead the internal order) has exactly 6 slots.
   h.deg6 = true;
-  for (int i = 0; i <= N && h.deg6; ++i) h.deg6 = off[i] == 6 * i;
+  for (int i = 0; i <= h.n_k1 && h.deg6; ++i) h.deg6 = off[i] == 6 * i;
   if (h.deg6) {
     std::vector<double4> sgeo(h.M);
     std::vector<double> sdx(3 * (size_t)h.M);
-    for (int i = 0; i < N; ++i)
+    for (int i = 0; i < h.n_k1; ++i)
       for (int t = 6 * i; t < 6 * i + 6; ++t) {
         const int j = adj_face[t] >= 0 ? adj_face[t] : ~adj_face[t];
         const double4 g = geo[j];
@@ -401,12 +573,19 @@ void alloc_state(tafv_gpu& h) {
   h.dtmax = dalloc<double>(N);
   h.nblk_dt = h.sms * 4;
   h.blockmin = dalloc<double>(h.nblk_dt);
-  h.ntile_c = (int)((N + kTile - 1) / kTile);
-  h.ntile_f = (int)((F + kTile - 1) / kTile);
-  h.cell_counts = dalloc<int>((size_t)h.ntile_c * kMaxLevels);
+  h.ntile_c = (int)((h.n_own + kTile - 1) / kTile);
+  h.ntile_f = (int)((h.F_own + kTile - 1) / kTile);
+  h.cell_counts = dalloc<int>((size_t)std::max(1, h.ntile_c) * kMaxLevels);
   h.face_counts = dalloc<int>((size_t)std::max(1, h.ntile_f) * kMaxLevels);
   h.clist = dalloc<int>(N);
   h.flist = dalloc<int>(F);
+  if (h.n_k1 != h.n_own) {
+    h.klist = dalloc<int>(N);
+    h.ntile_k = (int)((h.n_k1 + kTile - 1) / kTile);
+    h.k1_counts = dalloc<int>((size_t)std::max(1, h.ntile_k) * kMaxLevels);
+  } else {
+    h.klist = h.clist;
+  }
   h.nblk_last = h.sms * 16;
   h.partials = dalloc<DD>((size_t)h.nblk_last * 8);
   h.dplan = dalloc<PlanDev>(1);
@@ -476,13 +655,42 @@ void collect_times(tafv_gpu& h) {
   h.evkind.clear();
 }
 
+// ---- halo exchange (shards) -------------------------------------------------
+// Owned rows listed for the peers -> sendbuf -> comm -> recvbuf -> halo rows.
+void halo_rows(tafv_gpu& h, double* arr, int width) {
+  if (!h.sharded()) return;
+  if (h.send_total)
+    k_pack_rows<<<h.grid_for((long long)h.send_total * width, 256), 256, 0, h.st>>>(
+        arr, h.d_send_idx, h.send_total, width, h.sendbuf);
+  h.comm->exchange(h, width * (int)sizeof(double));
+  if (h.recv_total)
+    k_unpack_rows<<<h.grid_for((long long)h.recv_total * width, 256), 256, 0, h.st>>>(
+        h.recvbuf, h.d_recv_idx, h.recv_total, width, arr);
+  h.launches += 2;
+}
+
+void halo_i8(tafv_gpu& h, int8_t* arr) {
+  if (!h.sharded()) return;
+  int8_t* sb = reinterpret_cast<int8_t*>(h.sendbuf);
+  int8_t* rb = reinterpret_cast<int8_t*>(h.recvbuf);
+  if (h.send_total)
+    k_pack_i8<<<h.grid_for(h.send_total, 256), 256, 0, h.st>>>(arr, h.d_send_idx, h.send_total, sb);
+  h.comm->exchange(h, 1);
+  if (h.recv_total)
+    k_unpack_i8<<<h.grid_for(h.recv_total, 256), 256, 0, h.st>>>(rb, h.d_recv_idx, h.recv_total, arr);
+  h.launches += 2;
+}
+
 // ---- plan ------------------------------------------------------------------
 template <class P>
 void launch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
   k_dt_max<P><<<h.nblk_dt, 256, 0, h.st>>>(h.mesh_dev(), h.state_dev(), h.pp, cfl, dt_cap, h.dtmax,
-                                          h.blockmin, tau_scale);
+                                          h.blockmin, tau_scale, h.n_own);
   k_dt_min<<<1, 256, 0, h.st>>>(h.blockmin, h.nblk_dt, h.dplan);
   h.launches += 2;
+  // global stable step: exact min over ranks (RankComm::allreduce_min,
+  // exchange.cpp:155-192)
+  if (h.sharded()) h.comm->allreduce_min_f64(h.rank, &h.dplan->dt_min, 1, h.st);
 }
 
 void dispatch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
@@ -506,18 +714,31 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys) {
   const MeshDev md = h.mesh_dev();
   CK(cudaMemsetAsync(h.fflag, 0, h.N, h.st));
   k_face_cadence<<<h.grid_for(h.F, 256), 256, 0, h.st>>>(md, h.tau, h.cad, h.fflag, h.dplan);
-  k_tile_count<<<h.ntile_c, kCompactThreads, 0, h.st>>>(h.tau, h.N, nkeys, h.cell_counts, h.fflag, h.dplan);
-  k_tile_scan<<<1, 1024, 0, h.st>>>(h.cell_counts, h.ntile_c, nkeys, h.dplan->cell_count);
-  k_tile_scatter<<<h.ntile_c, kCompactThreads, 0, h.st>>>(h.tau, h.N, nkeys, h.cell_counts, h.clist);
+  // K3 list: owned cells by level (prefixes = active sets of each level)
+  k_tile_count<<<std::max(1, h.ntile_c), kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts,
+                                                                     h.fflag, h.dplan);
+  k_tile_scan<<<1, 1024, 0, h.st>>>(h.cell_counts, std::max(1, h.ntile_c), nkeys, h.dplan->cell_count);
+  k_tile_scatter<<<std::max(1, h.ntile_c), kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts,
+                                                                       h.clist);
   h.launches += 4;
-  if (h.F > 0) {
-    k_tile_count<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F, nkeys, h.face_counts, nullptr, h.dplan);
-    k_tile_scan<<<1, 1024, 0, h.st>>>(h.face_counts, h.ntile_f, nkeys, h.dplan->face_count);
-    k_tile_scatter<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F, nkeys, h.face_counts, h.flist);
+  if (h.klist != h.clist) {  // K1 list: owned + ring 1 by level (shards)
+    k_tile_count<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts,
+                                                                       nullptr, h.dplan);
+    k_tile_scan<<<1, 1024, 0, h.st>>>(h.k1_counts, std::max(1, h.ntile_k), nkeys, h.dplan->k1_count);
+    k_tile_scatter<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts,
+                                                                         h.klist);
     h.launches += 3;
   }
-  k_plan_prefix<<<1, 32, 0, h.st>>>(h.dplan);
+  if (h.F_own > 0) {  // K2 list: faces touching an owned cell by cadence
+    k_tile_count<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F_own, nkeys, h.face_counts, nullptr,
+                                                          h.dplan);
+    k_tile_scan<<<1, 1024, 0, h.st>>>(h.face_counts, h.ntile_f, nkeys, h.dplan->face_count);
+    k_tile_scatter<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F_own, nkeys, h.face_counts, h.flist);
+    h.launches += 3;
+  }
+  k_plan_prefix<<<1, 32, 0, h.st>>>(h.dplan, h.klist == h.clist ? 1 : 0);
   ++h.launches;
+  if (h.sharded()) h.comm->allreduce_sum_i64(h.rank, &h.dplan->gcell_count[0], kMaxLevels, h.st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
   h.plan_nkeys = nkeys;
@@ -546,7 +767,8 @@ void accept_plan(tafv_gpu& h) {
     h.ccount[l] = l < nkeys ? p.cell_count[l] : 0;
     h.fcount[l] = l < nkeys ? p.face_count[l] : 0;
     h.frcount[l] = p.fringe_count[l];
-    if (h.ccount[l] > 0) h.theta = l;
+    h.gcount[l] = l < nkeys ? p.gcell_count[l] : 0;
+    if (h.gcount[l] > 0) h.theta = l;  // theta = max level over all ranks
   }
   h.has_plan = true;
 }
@@ -559,9 +781,9 @@ void fill_plan_info(const tafv_gpu& h, tafv_plan_info* out) {
   out->dt = h.dt;
   long long cost = 0, fe = 0, re = 0;
   for (int l = 0; l <= h.theta; ++l) {
-    out->cells_per_level[l] = h.ccount[l];
+    out->cells_per_level[l] = h.gcount[l];
     out->faces_per_cadence[l] = h.fcount[l];
-    cost += (1ll << (h.theta - l)) * h.ccount[l];
+    cost += (1ll << (h.theta - l)) * h.gcount[l];
     fe += (1ll << (h.theta - l)) * h.fcount[l];
   }
   for (int l = 0; l < h.theta; ++l) {
@@ -572,7 +794,8 @@ void fill_plan_info(const tafv_gpu& h, tafv_plan_info* out) {
   out->f_eff = fe;
   out->r_eff = re;
   // LevelMap::cost_ratio (levels.cpp:73-79)
-  out->cost_ratio = cost == 0 ? 1.0 : (double)((1ll << h.theta) * (long long)h.N) / (double)cost;
+  const long long ncells = h.sharded() ? h.N_global : h.N;
+  out->cost_ratio = cost == 0 ? 1.0 : (double)((1ll << h.theta) * ncells) / (double)cost;
 }
 
 void plan_kernels(tafv_gpu& h, const tafv_options& opt);
@@ -585,7 +808,7 @@ void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
   require(h.state_set, "plan: state not set");
   h.has_plan = false;
   CK(cudaEventRecord(h.ev[2], h.st));
-  if (!h.use_graph || !h.plan_graph_on || h.ktime) {
+  if (!h.use_graph || !h.plan_graph_on || h.ktime || (h.sharded() && !h.comm->capturable())) {
     plan_kernels(h, opt);
   } else {
     const bool same = h.plan_graph && h.plan_opt.theta_max == opt.theta_max &&
@@ -617,20 +840,24 @@ void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
 void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
   dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr);
   reset_plan_counts(h);
-  k_classify<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.N, h.dtmax, h.dplan, opt.theta_max, h.raw);
+  k_classify<<<h.grid_for(h.n_own, 256), 256, 0, h.st>>>(h.n_own, h.dtmax, h.dplan, opt.theta_max, h.raw);
   ++h.launches;
+  halo_i8(h, h.raw);
   // Jacobi smoothing (levels.cpp:33-51). The fixpoint is
   // min_d raw(d) + dist(c, d); a cell more than theta_max hops away cannot
   // lower raw(c) <= theta_max, so theta_max sweeps reach it exactly.
   const MeshDev md = h.mesh_dev();
   if (opt.theta_max == 0) {
-    CK(cudaMemcpyAsync(h.tau, h.raw, h.N, cudaMemcpyDeviceToDevice, h.st));
+    CK(cudaMemcpyAsync(h.tau, h.raw, h.N, cudaMemcpyDeviceToDevice, h.st));  // raw halo already fresh
   } else {
+    // shards: sweep the owned cells, then refresh the halo levels (the
+    // replicated-array Jacobi of the reference, levels.hpp:32-37)
     const int8_t* src = h.raw;
     for (int i = 0; i < opt.theta_max; ++i) {
       int8_t* dst = i == opt.theta_max - 1 ? h.tau : (i % 2 == 0 ? h.tmpa : h.tmpb);
-      k_smooth<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(md, src, dst);
+      k_smooth<<<h.grid_for(h.n_own, 256), 256, 0, h.st>>>(md, src, dst, h.n_own);
       ++h.launches;
+      halo_i8(h, dst);
       src = dst;
     }
   }
@@ -653,12 +880,21 @@ void plan(tafv_gpu& h, const tafv_options& opt) {
   check_plan(h);
 }
 
-void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options* opt) {
+void inject(tafv_gpu& h, const int32_t* tau_in, double dt, const tafv_options* opt) {
   require(h.state_set || dt > 0.0, "inject_levels: state not set");
+  // shards take the GLOBAL level map and keep their local cells' entries
+  std::vector<int32_t> local;
+  const int32_t* tau_host = tau_in;
+  if (h.sharded()) {
+    local.resize(h.N);
+    for (int i = 0; i < h.N; ++i) local[i] = tau_in[h.shard_cells[i]];
+    tau_host = local.data();
+  }
   int maxl = 0;
-  for (int c = 0; c < h.N; ++c) {
-    require(tau_host[c] >= 0, "level map: negative level");
-    maxl = std::max(maxl, (int)tau_host[c]);
+  const int nchk = h.sharded() ? h.N_global : h.N;
+  for (int c = 0; c < nchk; ++c) {
+    require(tau_in[c] >= 0, "level map: negative level");
+    maxl = std::max(maxl, (int)tau_in[c]);
   }
   require(maxl < kMaxLevels, "level map: level above the supported 15");
   h.has_plan = false;
@@ -688,16 +924,20 @@ void inject(tafv_gpu& h, const int32_t* tau_host, double dt, const tafv_options*
 // ---- the subiteration sweep ------------------------------------------------
 template <class P, int DEG>
 void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
-  long long na = 0, nf = 0;
+  long long na = 0, nf = 0, nk = 0;
   for (int l = 0; l <= level; ++l) {
     na += h.ccount[l];
     nf += h.fcount[l];
   }
-  // Level theta activates every cell and face (tau <= theta): identity lists.
+  nk = h.klist == h.clist ? na : h.n_k1;  // shards: K1 over owned + ring 1 (upper bound)
+  // Level theta activates every cell and face (tau <= theta): identity lists
+  // (owned / owned + ring 1 / faces touching owned lead the internal order).
   const bool all = level == h.theta;
   const int* cl = all ? nullptr : h.clist;
+  const int* kl = all ? nullptr : h.klist;
   const int* fl = all ? nullptr : h.flist;
   const int* ncp = &h.dplan->ncell_prefix[level];
+  const int* nkp = &h.dplan->nk1_prefix[level];
   const int* nfp = &h.dplan->nface_prefix[level];
   const MeshDev md = h.mesh_dev();
   const StateDev sd = h.state_dev();
@@ -705,12 +945,12 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   // the counts); direct mode: grids sized from the host-known counts.
   const bool fixed = h.capturing;
   constexpr int CPB = (32 / P::NV) * 4;  // cells per 128-thread block in K3
-  const int g1 = fixed ? h.grid_k1 : h.grid_for(na, 128);
+  const int g1 = fixed ? h.grid_k1 : h.grid_for(nk, 128);
   const int g2 = fixed ? h.grid_k2 : h.grid_for(nf, 128);
   const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
   timed(h, tafv_gpu::kK1, [&] {
-    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, cl, ncp, front, pred ? 1 : 0);
+    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, front, pred ? 1 : 0);
   }, na, nf, nfr);
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan);
@@ -723,6 +963,11 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     }, na, nf, 0);
     k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan);
     h.launches += 4;
+    if (h.sharded()) {
+      h.comm->allreduce_sum_f64(h.rank, h.dplan->totals, P::NV, h.st);
+      h.comm->allreduce_max_i32(h.rank, &h.dplan->nonfinite, 1, h.st);
+    }
+    halo_rows(h, h.w, P::NV);  // the next iteration stages the halo's new w
   } else {
     timed(h, pred ? tafv_gpu::kK3P : tafv_gpu::kK3C, [&] {
       if (pred)
@@ -731,6 +976,9 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
         k_gather_update<P, false, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials);
     }, na, nf, 0);
     h.launches += 3;
+    // shards: the just-updated rows of owned cells to the peers' halos
+    // (w_pred after a predictor, w after a corrector)
+    halo_rows(h, pred ? h.wp : h.w, P::NV);
   }
 }
 
@@ -766,7 +1014,7 @@ void enqueue_sweep_direct(tafv_gpu& h) {
 // launch reads its active count and dt from the device plan, so the graph
 // captured once replays for every later iteration with the same theta.
 void run_sweep(tafv_gpu& h) {
-  if (!h.use_graph || h.ktime) {
+  if (!h.use_graph || h.ktime || (h.sharded() && !h.comm->capturable())) {
     enqueue_sweep_direct(h);
     return;
   }
@@ -812,7 +1060,7 @@ void close_iteration(tafv_gpu& h, tafv_record* rec) {
     rec->nv = h.nv;
     for (int k = 0; k < h.nv; ++k) rec->total_extensive[k] = h.hplan->totals[k];
     rec->n_levels = h.theta + 1;
-    for (int l = 0; l <= h.theta; ++l) rec->level_cells[l] = h.ccount[l];
+    for (int l = 0; l <= h.theta; ++l) rec->level_cells[l] = h.gcount[l];
   }
 }
 
@@ -845,8 +1093,9 @@ void integrate_pipelined(tafv_gpu& h, const tafv_options& opt, int n, tafv_recor
     // snapshot the plan that drives sweep i (the next plan overwrites h.*)
     const int theta = h.theta;
     const double dt = h.dt;
-    long long cc[kMaxLevels];
+    long long cc[kMaxLevels], gc[kMaxLevels];
     std::memcpy(cc, h.ccount, sizeof cc);
+    std::memcpy(gc, h.gcount, sizeof gc);
     run_sweep(h);
     const bool more = i + 1 < n;
     if (more) {
@@ -859,16 +1108,19 @@ void integrate_pipelined(tafv_gpu& h, const tafv_options& opt, int n, tafv_recor
     // close iteration i with its own plan
     const int th_next = h.theta;
     const double dt_next = h.dt;
-    long long cc_next[kMaxLevels];
+    long long cc_next[kMaxLevels], gc_next[kMaxLevels];
     std::memcpy(cc_next, h.ccount, sizeof cc_next);
+    std::memcpy(gc_next, h.gcount, sizeof gc_next);
     h.theta = theta;
     h.dt = dt;
     std::memcpy(h.ccount, cc, sizeof cc);
+    std::memcpy(h.gcount, gc, sizeof gc);
     close_iteration(h, (keep_all || !more) && out ? (keep_all ? out + i : out) : nullptr);
     if (more) {
       h.theta = th_next;
       h.dt = dt_next;
       std::memcpy(h.ccount, cc_next, sizeof cc_next);
+      std::memcpy(h.gcount, gc_next, sizeof gc_next);
       check_plan(h);
     }
   }
@@ -912,8 +1164,10 @@ int guard(tafv_gpu* h, F&& f) {
 
 extern "C" {
 
-int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
-                    tafv_gpu** out) {
+// Shared by tafv_gpu_create and tafv_gpu_create_shard. `shard` (optional)
+// makes the handle a rank of a decomposed run.
+static int create_handle(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
+                         const tafv::Shard* shard, tafv_comm* comm, int n_global, tafv_gpu** out) {
   if (!out || !mesh || !physics) {
     g_create_error = "tafv_gpu_create: null argument";
     return TAFV_EINVAL;
@@ -952,7 +1206,38 @@ int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int
     }
     if (h->model != TAFV_EULER) require(mesh->dim <= 2, "physics: scalar models run on 1D/2D meshes");
     else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
-    upload_mesh(*h, *mesh);
+    if (shard) {
+      std::vector<uint8_t> touch(shard->touch_own.begin(), shard->touch_own.end());
+      upload_mesh(*h, *mesh, shard->cls.data(), touch.data());
+      h->comm = comm;
+      h->rank = shard->rank;
+      h->nranks = shard->nranks;
+      h->N_global = n_global;
+      h->shard_cells = shard->cells;
+      // exchange lists in internal ids, peer segments in shard order
+      std::vector<int> cinv(h->N);
+      for (int i = 0; i < h->N; ++i) cinv[h->cperm[i]] = i;
+      std::vector<int> sidx, ridx;
+      for (size_t p = 0; p < shard->peers.size(); ++p) {
+        tafv_gpu::Peer pe{shard->peers[p], (int)shard->send[p].size(), (int)shard->recv[p].size(),
+                          (int)sidx.size(), (int)ridx.size()};
+        for (int c : shard->send[p]) sidx.push_back(cinv[c]);
+        for (int c : shard->recv[p]) ridx.push_back(cinv[c]);
+        h->peers.push_back(pe);
+      }
+      h->send_total = (int)sidx.size();
+      h->recv_total = (int)ridx.size();
+      h->d_send_idx = dalloc<int>(sidx.size());
+      h->d_recv_idx = dalloc<int>(ridx.size());
+      if (!sidx.empty()) CK(cudaMemcpy(h->d_send_idx, sidx.data(), sidx.size() * 4, cudaMemcpyHostToDevice));
+      if (!ridx.empty()) CK(cudaMemcpy(h->d_recv_idx, ridx.data(), ridx.size() * 4, cudaMemcpyHostToDevice));
+      const int width = std::max(h->nv, 1);
+      h->sendbuf = dalloc<double>((size_t)std::max(1, h->send_total) * width);
+      h->recvbuf = dalloc<double>((size_t)std::max(1, h->recv_total) * width);
+      comm->attach(h->rank, h);
+    } else {
+      upload_mesh(*h, *mesh);
+    }
     alloc_state(*h);
     set_grids(*h);
   } catch (const Error& e) {
@@ -968,15 +1253,82 @@ int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int
   return TAFV_OK;
 }
 
+int tafv_gpu_create(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
+                    tafv_gpu** out) {
+  return create_handle(mesh, physics, device, nullptr, nullptr, 0, out);
+}
+
+int tafv_comm_create_loopback(int32_t nranks, tafv_comm** out) {
+  if (!out || nranks < 1) return TAFV_EINVAL;
+  *out = make_loopback_comm(nranks);
+  return TAFV_OK;
+}
+
+int tafv_comm_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return TAFV_EINVAL;
+  return nccl_unique_id(out128);
+}
+
+int tafv_comm_create_nccl(const uint8_t* id128, int32_t rank, int32_t nranks, int device,
+                          tafv_comm** out) {
+  if (!out || !id128 || rank < 0 || rank >= nranks) return TAFV_EINVAL;
+  try {
+    CK(cudaSetDevice(device));
+    *out = make_nccl_comm(id128, rank, nranks);
+  } catch (const Error& e) {
+    g_create_error = e.what;
+    return e.code;
+  }
+  return TAFV_OK;
+}
+
+void tafv_comm_destroy(tafv_comm* c) { delete c; }
+
+int tafv_gpu_create_shard(const tafv_mesh_view* global_mesh, const tafv_physics* physics, int device,
+                          const int32_t* rank_of_cell, int32_t rank, tafv_comm* comm, tafv_gpu** out) {
+  if (!global_mesh || !rank_of_cell || !comm || !out) {
+    g_create_error = "tafv_gpu_create_shard: null argument";
+    return TAFV_EINVAL;
+  }
+  try {
+    const tafv::Shard sh = tafv::build_shard(*global_mesh, rank_of_cell, rank, comm->nranks());
+    const tafv_mesh_view lv = sh.view(global_mesh->dim);
+    return create_handle(&lv, physics, device, &sh, comm, global_mesh->n_cells, out);
+  } catch (const std::invalid_argument& e) {
+    g_create_error = e.what();
+    return TAFV_EINVAL;
+  } catch (const std::exception& e) {
+    g_create_error = e.what();
+    return TAFV_ELOGIC;
+  }
+}
+
 void tafv_gpu_destroy(tafv_gpu* h) { delete h; }
 
 const char* tafv_gpu_last_error(const tafv_gpu* h) {
   return h ? h->err.c_str() : g_create_error.c_str();
 }
 
-int tafv_gpu_set_state(tafv_gpu* h, const double* w, const double* W, double t0, int32_t iteration) {
+int tafv_gpu_set_state(tafv_gpu* h, const double* w_in, const double* W_in, double t0,
+                       int32_t iteration) {
   return guard(h, [&] {
-    require(w != nullptr, "set_state: w is null");
+    require(w_in != nullptr, "set_state: w is null");
+    // shards take the GLOBAL state and keep their local cells' rows
+    std::vector<double> wl, Wl;
+    const double* w = w_in;
+    const double* W = W_in;
+    if (h->sharded()) {
+      wl.resize((size_t)h->N * h->nv);
+      for (int i = 0; i < h->N; ++i)
+        std::memcpy(&wl[(size_t)i * h->nv], w_in + (size_t)h->shard_cells[i] * h->nv, h->nv * sizeof(double));
+      w = wl.data();
+      if (W_in) {
+        Wl.resize(wl.size());
+        for (int i = 0; i < h->N; ++i)
+          std::memcpy(&Wl[(size_t)i * h->nv], W_in + (size_t)h->shard_cells[i] * h->nv, h->nv * sizeof(double));
+        W = Wl.data();
+      }
+    }
     const size_t n = (size_t)h->N * h->nv;
     double* stage = h->staging(n);
     CK(cudaMemcpyAsync(stage, w, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
@@ -996,9 +1348,23 @@ int tafv_gpu_set_state(tafv_gpu* h, const double* w, const double* W, double t0,
   });
 }
 
-int tafv_gpu_get_state(tafv_gpu* h, double* w, double* W, double* t0, int32_t* iteration) {
+int tafv_gpu_get_state(tafv_gpu* h, double* w_out, double* W_out, double* t0, int32_t* iteration) {
   return guard(h, [&] {
     const size_t n = (size_t)h->N * h->nv;
+    // shards write their OWNED rows into the global arrays
+    std::vector<double> wl, Wl;
+    double* w = w_out;
+    double* W = W_out;
+    if (h->sharded()) {
+      if (w_out) {
+        wl.resize(n);
+        w = wl.data();
+      }
+      if (W_out) {
+        Wl.resize(n);
+        W = Wl.data();
+      }
+    }
     double* stage = h->staging(n);
     if (w) {
       k_scatter_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->w, h->d_cperm, h->N, h->nv, stage);
@@ -1009,6 +1375,16 @@ int tafv_gpu_get_state(tafv_gpu* h, double* w, double* W, double* t0, int32_t* i
       CK(cudaMemcpyAsync(W, stage, n * sizeof(double), cudaMemcpyDeviceToHost, h->st));
     }
     CK(cudaStreamSynchronize(h->st));
+    if (h->sharded()) {
+      std::vector<int> cinv(h->N);
+      for (int i = 0; i < h->N; ++i) cinv[h->cperm[i]] = i;
+      for (int c = 0; c < h->N; ++c) {
+        if (cinv[c] >= h->n_own) continue;  // owned cells lead the internal order
+        const size_t g = (size_t)h->shard_cells[c] * h->nv;
+        if (w_out) std::memcpy(w_out + g, &wl[(size_t)c * h->nv], h->nv * sizeof(double));
+        if (W_out) std::memcpy(W_out + g, &Wl[(size_t)c * h->nv], h->nv * sizeof(double));
+      }
+    }
     if (t0) *t0 = h->t0;
     if (iteration) *iteration = h->iteration;
   });

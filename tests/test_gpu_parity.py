@@ -240,3 +240,89 @@ def test_cpp_shim_caller(gpu):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "cpp_shim_check ok" in r.stdout
+
+
+def _sharded_run(cfg, world, iters, axis=0, use_graph=1):
+    """`world` loopback ranks as host threads on one GPU (tafv_gpu_create_shard)."""
+    import threading
+
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    roc = shard.partition_slabs(mesh, world, axis=axis)
+    comm = Comm.loopback(world)
+    out, errs = {}, []
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(world)]
+
+    def body(r):
+        try:
+            s = solvers[r]
+            s.set_flag("use_graph", use_graph)
+            s.set_state(w0)
+            recs = s.reference_integrate(cfg.options(), iters)
+            w, W, t0, it = s.get_state()
+            out[r] = (recs, w, W, t0, it)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for s in solvers:
+        s.close()
+    comm.close()
+    assert not errs, errs
+    w = sum(out[r][1] * (roc == r)[:, None] for r in range(world))
+    W = sum(out[r][2] * (roc == r)[:, None] for r in range(world))
+    return mesh, w0, out, w, W
+
+
+@pytest.mark.parametrize("cid,scale,world,iters,axis", [(2, 5, 2, 4, 0), (3, 10, 3, 3, 1), (4, 20, 2, 2, 0),
+                                                        (1, 4, 4, 6, 2)])
+def test_sharded_loopback_matches_single_domain_bitwise(cid, scale, world, iters, axis, gpu):
+    """The CUDA shard path (2-ring halo, per-phase exchange, duplicated
+    interface faces, dt/theta/count collectives) run as `world` ranks on one
+    GPU reproduces the single-domain GPU run bitwise, records included."""
+    cfg = configs.get(cid, scale)
+    mesh, w0, out, w, W = _sharded_run(cfg, world, iters, axis)
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    ref = g.reference_integrate(cfg.options(), iters)
+    wr, Wr, t0r, itr = g.get_state()
+    np.testing.assert_array_equal(w, wr)
+    np.testing.assert_array_equal(W, Wr)
+    for r in range(world):
+        recs, _, _, t0, it = out[r]
+        assert (t0, it) == (t0r, itr)
+        assert [x["dt"] for x in recs] == [x["dt"] for x in ref]
+        assert [x["level_cells"] for x in recs] == [x["level_cells"] for x in ref]
+        assert [x["cost_ratio"] for x in recs] == [x["cost_ratio"] for x in ref]
+        for a, b in zip(recs, ref):
+            for x, y in zip(a["total_extensive"], b["total_extensive"]):
+                assert abs(x - y) <= 1e-12 * max(1.0, abs(y))
+
+
+def test_nccl_single_rank_shard(gpu):
+    """NCCL communicator end to end on the one GPU available here: a 1-rank
+    shard (no peers) runs the graph-captured plan/sweep with the NCCL
+    all-reduces inside and matches the plain handle bitwise."""
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    cfg = configs.get(2, 5)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    comm = Comm.nccl(Comm.nccl_unique_id(), 0, 1)
+    s = Solver(mesh, "euler", shard=(np.zeros(len(mesh["vol"]), dtype=np.int32), 0, comm))
+    s.set_state(w0)
+    rs = s.reference_integrate(cfg.options(), 4)
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    rg = g.reference_integrate(cfg.options(), 4)
+    np.testing.assert_array_equal(s.get_state()[0], g.get_state()[0])
+    assert [x["dt"] for x in rs] == [x["dt"] for x in rg]
+    s.close()
+    comm.close()
+    del shard
