@@ -56,6 +56,7 @@ class Config:
     seed: int
     dt_cap: float = 1e30
     synthetic_levels: float | None = None  # tau=0 fraction for config 5
+    tiles: int = 1  # weak-scaling copies of the unit-cube config along x
     extra: dict = field(default_factory=dict)
 
     @property
@@ -65,18 +66,24 @@ class Config:
     def nodes(self):
         axes = []
         for d, n in enumerate(self.n):
-            g, a = self.grading, self.grading_args
-            if g == "uniform":
-                axes.append(meshgen.uniform_nodes(n))
-            elif g == "centre":
-                axes.append(meshgen.centre_graded_nodes(n, *a))
-            elif g == "corner":
-                axes.append(meshgen.geometric_nodes(n, a[0]))
-            elif g == "wall_z":
-                axes.append(meshgen.geometric_nodes(n, a[0]) if d == 2 else meshgen.uniform_nodes(n))
-            else:
-                raise ValueError(g)
+            if d == 0 and self.tiles > 1:  # tiles copies of the x grading over [0, tiles]
+                one = self._axis(0, n // self.tiles)
+                axes.append(np.concatenate([one[:-1] + t for t in range(self.tiles)] + [[float(self.tiles)]]))
+                continue
+            axes.append(self._axis(d, n))
         return axes
+
+    def _axis(self, d, n):
+        g, a = self.grading, self.grading_args
+        if g == "uniform":
+            return meshgen.uniform_nodes(n)
+        if g == "centre":
+            return meshgen.centre_graded_nodes(n, *a)
+        if g == "corner":
+            return meshgen.geometric_nodes(n, a[0])
+        if g == "wall_z":
+            return meshgen.geometric_nodes(n, a[0]) if d == 2 else meshgen.uniform_nodes(n)
+        raise ValueError(g)
 
     def mesh(self):
         x, y, z = self.nodes()
@@ -89,9 +96,11 @@ class Config:
             left = c[:, 0] < 0.5
             rho = np.where(left, 1.0, 0.125)
             p = np.where(left, 1.0, 0.1)
-        else:  # blast
-            r2 = ((c - np.asarray(a["centre"])) ** 2).sum(axis=1)
-            inside = r2 < a["radius"] ** 2
+        else:  # blast (one per tile)
+            inside = np.zeros(len(c), dtype=bool)
+            for t in range(self.tiles):
+                ctr = np.asarray(a["centre"], dtype=np.float64) + np.array([t, 0.0, 0.0])
+                inside |= ((c - ctr) ** 2).sum(axis=1) < a["radius"] ** 2
             rho = np.where(inside, a["rho_in"], 1.0)
             p = np.where(inside, a["p_in"], 1.0)
         return euler_conserved(rho, p)
@@ -114,6 +123,18 @@ class Config:
         qs = np.quantile(s, [f0, f0 + (1 - f0) / 3, f0 + 2 * (1 - f0) / 3])
         tau = np.minimum(np.searchsorted(qs, s, side="right"), self.theta_max).astype(np.int32)
         return smooth_to_fixpoint(mesh, tau)
+
+    def tiled(self, n):
+        """Weak-scaling workload: n copies of this config side by side along x
+        (domain [0, n] x [0, 1]^2, one blast per copy): every slab rank of an
+        n-GPU run owns one copy's worth of cells and work."""
+        import copy
+        c = copy.deepcopy(self)
+        if n > 1:
+            c.tiles = n
+            c.n = (self.n[0] * n, self.n[1], self.n[2])
+            c.name = f"{self.name}-x{n}"
+        return c
 
     def scaled(self, factor):
         """Same config at resolution n / factor (for CPU parity runs)."""
