@@ -1,0 +1,144 @@
+#!/usr/bin/env python3
+"""Summarise a round's ncu evidence (gpurun_out/) into profiles/.
+
+    python tools/summarize_ncu.py r1
+
+Writes profiles/<tag>_launches.md (every launch of the profiled bench
+command, grouped by kernel: count, total time, share of kernel time),
+profiles/<tag>_kernels.md (full-set metrics of one iteration's worth of each
+hot kernel) and profiles/ncu_traffic.json (average DRAM bytes per launch per
+bench kernel kind, read by bench.py for roofline.traffic)."""
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+KIND = [  # bench.py kernel kind <- short ncu name prefixes
+    ("K1_grad_limit", "k_grad_limit<"),
+    ("K2_face_pred", "k_face_flux<Euler3D, 1>"),
+    ("K2_face_corr", "k_face_flux<Euler3D, 0>"),
+    ("K3_update_pred", "k_gather_update<Euler3D, 1, 0"),
+    ("K3_update_corr", "k_gather_update<Euler3D, 0"),
+]
+
+UNIT = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9,
+        "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def kind_of(name):
+    n = short(name)
+    for k, frag in KIND:
+        if n.startswith(frag):
+            return k
+    return None
+
+
+def short(name):
+    return name.replace("void ", "").replace("tafv::", "").split("(")[0]
+
+
+def launches(tag):
+    rows = [r for r in csv.reader(open(os.path.join(OUT, f"launches_{tag}.csv"))) if len(r) > 5]
+    hdr = rows[0]
+    i_n, i_v = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = collections.OrderedDict()
+    for r in rows[1:]:
+        agg.setdefault(short(r[i_n]), []).append(float(r[i_v].replace(",", "")) / 1e3)
+    tot = sum(sum(v) for v in agg.values())
+    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1`",
+             "", "`ncu --metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised",
+             "launches: compare SHARES with bench.py's event-timed breakdown, not absolutes).", "",
+             "| kernel | launches | total us | share of kernel time | avg us |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v) / tot * 100:.1f} % | {sum(v) / len(v):.1f} |")
+    lines.append(f"| **all** | {sum(len(v) for v in agg.values())} | {tot:.1f} | 100 % | |")
+    return "\n".join(lines) + "\n"
+
+
+METRICS = [  # (metric, column, scale from base units: ns / bytes)
+    ("gpu__time_duration.sum", "duration (us)", 1e-3),
+    ("dram__bytes_read.sum", "DRAM read (MB)", 1e-6),
+    ("dram__bytes_write.sum", "DRAM write (MB)", 1e-6),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak", 1),
+    ("launch__registers_per_thread", "regs/thread", 1),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %", 1),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %", 1),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe %", 1),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %", 1),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %", 1),
+    ("launch__grid_size", "grid", 1),
+]
+
+
+def raw_rows(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    return rows[0], rows[1], rows[2:]
+
+
+def val(r, hdr, units, m):
+    """Metric value in base units (ns, bytes) using the CSV unit row."""
+    if m not in hdr:
+        return None
+    i = hdr.index(m)
+    try:
+        v = float(r[i].replace(",", ""))
+    except ValueError:
+        return None
+    return v * UNIT.get(units[i], 1.0)
+
+
+def full(tag):
+    lines = [f"# {tag}: ncu --set full, one iteration's worth of launches per hot kernel", "",
+             "`ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 40 -c 8` on",
+             "the same bench command (cache flushed between replays: cold-cache numbers).", ""]
+    traffic = {}
+    for k in ("k_grad_limit", "k_face_flux", "k_gather_update"):
+        rep = os.path.join(OUT, f"full_{tag}_{k}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        hdr, units, rows = raw_rows(rep)
+        lines += [f"## `{k}`", "", "| launch | kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls (cycles/issue) |",
+                  "|---" * (len(METRICS) + 3) + "|"]
+        for i, r in enumerate(rows):
+            name = r[hdr.index("Kernel Name")]
+            vals = []
+            for m, _, sc in METRICS:
+                v = val(r, hdr, units, m)
+                vals.append("-" if v is None else f"{v * sc:.1f}")
+            st = sorted(((h.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""),
+                          float(r[j] or 0)) for j, h in enumerate(hdr)
+                         if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("per_issue_active.ratio")),
+                        key=lambda x: -x[1])[:3]
+            lines.append(f"| {i} | `{short(name)}` | " + " | ".join(vals) + " | " +
+                         ", ".join(f"{a} {b:.1f}" for a, b in st) + " |")
+            kind = kind_of(name)
+            if kind:
+                b = val(r, hdr, units, "dram__bytes_read.sum") + val(r, hdr, units, "dram__bytes_write.sum")
+                traffic.setdefault(kind, []).append(b)
+        lines.append("")
+    tj = {k: {"bytes_per_launch": sum(v) / len(v), "launches": len(v),
+              "source": f"profiles/{tag}_kernels.md (ncu --set full, cold cache, mean over the captured launches)"}
+          for k, v in traffic.items()}
+    return "\n".join(lines) + "\n", tj
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    os.makedirs(PROF, exist_ok=True)
+    open(os.path.join(PROF, f"{tag}_launches.md"), "w").write(launches(tag))
+    md, tj = full(tag)
+    open(os.path.join(PROF, f"{tag}_kernels.md"), "w").write(md)
+    json.dump(tj, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+    print(json.dumps(tj, indent=1))
+
+
+if __name__ == "__main__":
+    main()
