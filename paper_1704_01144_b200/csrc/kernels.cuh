@@ -125,19 +125,13 @@ __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0;
 //   delta NaN                      -> NaN ratio: smin leaves alpha unchanged;
 //   delta == 0                     -> skipped by the reference.
 __device__ __forceinline__ double bj_update(double alpha, double delta, double head) {
-  if (delta > 0.0) {
-    if (head > 0.0) {
-      if (head < delta) alpha = smin(alpha, head / delta);
-    } else {
-      alpha = smin(alpha, 0.0);
-    }
-  } else if (delta < 0.0) {
-    if (head < 0.0) {
-      if (delta < head) alpha = smin(alpha, head / delta);
-    } else {
-      alpha = smin(alpha, -0.0);
-    }
-  }
+  // zero outcome (opposite signs, head == 0 or NaN): +0 for delta > 0, -0 for
+  // delta < 0 -- predicated; the quotient only where |head| < |delta|.
+  const bool pos = delta > 0.0, neg = delta < 0.0;
+  const bool same = pos ? head > 0.0 : head < 0.0;
+  const bool lim = same && (pos ? head < delta : delta < head);
+  if ((pos || neg) && !same) alpha = smin(alpha, pos ? 0.0 : -0.0);
+  if (lim) alpha = smin(alpha, head / delta);
   return alpha;
 }
 
@@ -191,7 +185,11 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       double wf[NV];
       if (nb >= 0) {
         double wn[NV];
+#ifdef TAFV_EXP_NO_GATHER
+        for (int k = 0; k < NV; ++k) wn[k] = we[k] * (1.0 + 1e-3 * t);  // timing experiment only
+#else
         stage<NV>(s, nb, s.tau[nb], front, pred, wn);
+#endif
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
           wf[k] = 0.5 * (we[k] + wn[k]);
@@ -215,12 +213,20 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
     for (int k = 0; k < NV; ++k)
 #pragma unroll
       for (int d = 0; d < D; ++d) g[k][d] = g[k][d] * inv_v;
+#ifdef TAFV_EXP_NO_LIMIT
+    any = false;  // timing experiment only
+#endif
     if (any) {
       const double* cp = m.cen + 3 * (size_t)c;
       const double cc0 = cp[0], cc1 = cp[1], cc2 = cp[2];
       double alpha[NV];
+      // headroom operands are the same for every slot (kernels.cpp:115-116)
 #pragma unroll
-      for (int k = 0; k < NV; ++k) alpha[k] = 1.0;
+      for (int k = 0; k < NV; ++k) {
+        alpha[k] = 1.0;
+        wmax[k] = wmax[k] - we[k];
+        wmin[k] = wmin[k] - we[k];
+      }
 #pragma unroll
       for (int t = s0; t < s1; ++t) {
         double dx0, dx1, dx2;
@@ -240,9 +246,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
         for (int k = 0; k < NV; ++k) {
           double delta = g[k][0] * dx0 + g[k][1] * dx1;
           if (D == 3) delta = delta + g[k][D - 1] * dx2;
-          if (delta == 0.0) continue;
-          const double head = delta > 0.0 ? wmax[k] - we[k] : wmin[k] - we[k];
-          alpha[k] = bj_update(alpha[k], delta, head);
+          alpha[k] = bj_update(alpha[k], delta, delta > 0.0 ? wmax[k] : wmin[k]);
         }
       }
 #pragma unroll
