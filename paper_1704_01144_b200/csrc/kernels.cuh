@@ -97,18 +97,19 @@ __device__ __forceinline__ void stage(const StateDev& s, int x, int tx, int fron
                                       double* out) {
   const int win = 1 << tx;
   const int off = front & (win - 1);
+  // read-only within K1/K2 (only K3 writes w / w_pred): non-coherent path
   const double* w = s.w + (size_t)x * NV;
   const double* wp = s.wp + (size_t)x * NV;
   if (off == 0) {
     const double* src = pred ? w : wp;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) out[k] = src[k];
+    for (int k = 0; k < NV; ++k) out[k] = __ldg(src + k);
   } else {
     const double th = (double)off / (double)win;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const double a = w[k];
-      out[k] = a + th * (wp[k] - a);
+      const double a = __ldg(w + k);
+      out[k] = a + th * (__ldg(wp + k) - a);
     }
   }
 }
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int c = list ? list[i] : i;
     double we[NV];
-    stage<NV>(s, c, s.tau[c], front, pred, we);
+    stage<NV>(s, c, __ldg(s.tau + c), front, pred, we);
     double g[NV][D];
     double wmin[NV], wmax[NV];
 #pragma unroll
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #ifdef TAFV_EXP_NO_GATHER
         for (int k = 0; k < NV; ++k) wn[k] = we[k] * (1.0 + 1e-3 * t);  // timing experiment only
 #else
-        stage<NV>(s, nb, s.tau[nb], front, pred, wn);
+        stage<NV>(s, nb, __ldg(s.tau + nb), front, pred, wn);
 #endif
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -268,8 +269,9 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 template <int D>
 __device__ __forceinline__ double extrapolate(double w, const double* g, const double* from,
                                               const double* to) {
-  double v = (w + g[0] * (to[0] - from[0])) + g[1] * (to[1] - from[1]);
-  if (D == 3) v = v + g[D - 1] * (to[D - 1] - from[D - 1]);
+  // g: a gradient row, read-only in K2 (only K1 writes it)
+  double v = (w + __ldg(g) * (to[0] - from[0])) + __ldg(g + 1) * (to[1] - from[1]);
+  if (D == 3) v = v + __ldg(g + D - 1) * (to[D - 1] - from[D - 1]);
   return v;
 }
 
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     const double4 gm = m.geo[f];
     const double nrm[3] = {gm.x, gm.y, gm.z};
     const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
-    const int tl = s.tau[lr.x];
+    const int tl = __ldg(s.tau + lr.x);
     double wL[NV], wR[NV];
     {
       double we[NV];
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     }
     bool shared_start = (front & ((1 << tl) - 1)) == 0;
     if (lr.y >= 0) {
-      const int tr = s.tau[lr.y];
+      const int tr = __ldg(s.tau + lr.y);
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
       double we[NV];
       stage<NV>(s, lr.y, tr, front, PRED, we);
@@ -399,7 +401,7 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
   if (lane_ok) {
     for (int i = warp * CPW + j; i < n; i += nwarps * CPW) {
       const int c = list ? list[i] : i;
-      const int tc = s.tau[c];
+      const int tc = __ldg(s.tau + c);
       double sum = 0.0;
       const int s0 = DEG ? DEG * c : m.adj_off[c];
       const int s1 = DEG ? s0 + DEG : m.adj_off[c + 1];
