@@ -24,6 +24,7 @@
 #include <mutex>
 #include <cstdint>
 #include <cstring>
+#include <array>
 #include <map>
 #include <numeric>
 #include <stdexcept>
@@ -99,8 +100,19 @@ struct tafv_gpu {
   // Launch shapes: grid-stride kernels with a fixed, occupancy-sized grid
   // (graph mode) so the captured sweep of a theta never changes.
   bool use_graph = true;
-  std::map<int, cudaGraphExec_t> graphs;  // theta -> instantiated sweep
-  std::map<int, int64_t> graph_launches;  // kernels inside each graph
+  // theta (x2 + kernel_timing) -> instantiated sweep graph. With kernel
+  // timing on, event-record nodes bracket every hot kernel INSIDE the graph,
+  // so the instrumented replay runs exactly like the timed one.
+  struct GraphRec {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+    std::vector<int> kinds;
+    std::vector<std::array<long long, 3>> items;
+    std::vector<cudaEvent_t> evs;  // 2 per timed kernel
+  };
+  std::map<int, GraphRec> graphs;
+  GraphRec* cap = nullptr;            // record being captured
+  GraphRec* pending_graph = nullptr;  // replayed graph whose events await collection
   cudaGraphExec_t plan_graph = nullptr;   // plan_iteration for plan_opt
   bool plan_graph_on = true;
   tafv_options plan_opt{};
@@ -203,7 +215,10 @@ struct tafv_gpu {
 
   ~tafv_gpu() {
     cudaSetDevice(device);
-    for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+    for (auto& g : graphs) {
+      cudaGraphExecDestroy(g.second.exec);
+      for (auto e : g.second.evs) cudaEventDestroy(e);
+    }
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
     void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
@@ -629,6 +644,21 @@ void timed(tafv_gpu& h, int kind, F&& launch, long long cells = 0, long long fac
     launch();
     return;
   }
+  if (h.cap) {  // inside a graph capture: dedicated events become graph nodes
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    // external records: real event-record nodes (a plain record inside a
+    // capture only expresses a dependency and carries no timestamp)
+    CK(cudaEventRecordWithFlags(a, h.st, cudaEventRecordExternal));
+    launch();
+    CK(cudaEventRecordWithFlags(b, h.st, cudaEventRecordExternal));
+    h.cap->evs.push_back(a);
+    h.cap->evs.push_back(b);
+    h.cap->kinds.push_back(kind);
+    h.cap->items.push_back({cells, faces, fringe});
+    return;
+  }
   h.kitems[kind][0] += cells;
   h.kitems[kind][1] += faces;
   h.kitems[kind][2] += fringe;
@@ -646,6 +676,17 @@ void timed(tafv_gpu& h, int kind, F&& launch, long long cells = 0, long long fac
 
 // After a host sync: fold the recorded pairs into the per-kind totals.
 void collect_times(tafv_gpu& h) {
+  if (h.pending_graph) {
+    const auto& g = *h.pending_graph;
+    for (size_t i = 0; i < g.kinds.size(); ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, g.evs[2 * i], g.evs[2 * i + 1]));
+      h.kms[g.kinds[i]] += ms;
+      h.kcnt[g.kinds[i]] += 1;
+      for (int j = 0; j < 3; ++j) h.kitems[g.kinds[i]][j] += g.items[i][j];
+    }
+    h.pending_graph = nullptr;
+  }
   for (size_t i = 0; i < h.evkind.size(); ++i) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h.evpool[2 * i], h.evpool[2 * i + 1]));
@@ -808,7 +849,7 @@ void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
   require(h.state_set, "plan: state not set");
   h.has_plan = false;
   CK(cudaEventRecord(h.ev[2], h.st));
-  if (!h.use_graph || !h.plan_graph_on || h.ktime || (h.sharded() && !h.comm->capturable())) {
+  if (!h.use_graph || !h.plan_graph_on || (h.sharded() && !h.comm->capturable())) {
     plan_kernels(h, opt);
   } else {
     const bool same = h.plan_graph && h.plan_opt.theta_max == opt.theta_max &&
@@ -1014,29 +1055,33 @@ void enqueue_sweep_direct(tafv_gpu& h) {
 // launch reads its active count and dt from the device plan, so the graph
 // captured once replays for every later iteration with the same theta.
 void run_sweep(tafv_gpu& h) {
-  if (!h.use_graph || h.ktime || (h.sharded() && !h.comm->capturable())) {
+  if (!h.use_graph || (h.sharded() && !h.comm->capturable())) {
     enqueue_sweep_direct(h);
     return;
   }
-  auto it = h.graphs.find(h.theta);
+  const int key = 2 * h.theta + (h.ktime ? 1 : 0);
+  auto it = h.graphs.find(key);
   if (it == h.graphs.end()) {
+    tafv_gpu::GraphRec rec;
     cudaGraph_t g;
     h.capturing = true;
+    h.cap = &rec;
     const int64_t l0 = h.launches;
     CK(cudaStreamBeginCapture(h.st, cudaStreamCaptureModeThreadLocal));
     enqueue_sweep_direct(h);
     const cudaError_t e = cudaStreamEndCapture(h.st, &g);
     h.capturing = false;
+    h.cap = nullptr;
     CK(e);
-    cudaGraphExec_t ex;
-    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphInstantiate(&rec.exec, g, 0));
     CK(cudaGraphDestroy(g));
-    it = h.graphs.emplace(h.theta, ex).first;
-    h.graph_launches[h.theta] = h.launches - l0;
+    rec.launches = h.launches - l0;
     h.launches = l0;
+    it = h.graphs.emplace(key, std::move(rec)).first;
   }
-  CK(cudaGraphLaunch(it->second, h.st));
-  h.launches += h.graph_launches[h.theta];
+  CK(cudaGraphLaunch(it->second.exec, h.st));
+  h.launches += it->second.launches;
+  if (h.ktime) h.pending_graph = &it->second;
 }
 
 void close_iteration(tafv_gpu& h, tafv_record* rec) {
@@ -1518,7 +1563,10 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
     } else if (n == "slot_geo") {
       h->slot_geo = value != 0;
-      for (auto& g : h->graphs) cudaGraphExecDestroy(g.second);
+      for (auto& g : h->graphs) {
+        cudaGraphExecDestroy(g.second.exec);
+        for (auto e : g.second.evs) cudaEventDestroy(e);
+      }
       h->graphs.clear();
     } else if (n == "plan_graph") {
       h->plan_graph_on = value != 0;
