@@ -150,11 +150,14 @@ template <class P, int DEG>
 __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, StateDev s,
                                                     const int* __restrict__ list,
                                                     const int* __restrict__ n_dev, int front,
-                                                    int pred) {
+                                                    int pred, int rev) {
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+    // rev: walk the items backwards, so this kernel starts on the rows its
+    // predecessor wrote last (still in L2); consecutive kernels alternate.
+    const int i = rev ? n - 1 - ii : ii;
     const int c = list ? list[i] : i;
     double we[NV];
     stage<NV>(s, c, __ldg(s.tau + c), front, pred, we);
@@ -283,12 +286,13 @@ template <class P, bool PRED>
 __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
                                                    const int* __restrict__ list,
                                                    const int* __restrict__ n_dev, int front,
-                                                   const PlanDev* __restrict__ plan) {
+                                                   const PlanDev* __restrict__ plan, int rev) {
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
   const double dt = plan->dt_min;
   const int stride = gridDim.x * blockDim.x;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+    const int i = rev ? n - 1 - ii : ii;
     const int f = list ? list[i] : i;
     const int2 lr = m.lr[f];
     const double4 gm = m.geo[f];
@@ -387,7 +391,7 @@ template <class P, bool PRED, bool LAST, int DEG>
 __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
                                                        const int* __restrict__ list,
                                                        const int* __restrict__ n_dev,
-                                                       PlanDev* plan, DD* partials) {
+                                                       PlanDev* plan, DD* partials, int rev) {
   constexpr int NV = P::NV, CPW = 32 / NV;
   const int n = *n_dev;
   const double dt = plan->dt_min;
@@ -399,7 +403,8 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
   DD acc{0.0, 0.0};
   bool bad = false;
   if (lane_ok) {
-    for (int i = warp * CPW + j; i < n; i += nwarps * CPW) {
+    for (int ii = warp * CPW + j; ii < n; ii += nwarps * CPW) {
+      const int i = rev ? n - 1 - ii : ii;
       const int c = list ? list[i] : i;
       const int tc = __ldg(s.tau + c);
       double sum = 0.0;

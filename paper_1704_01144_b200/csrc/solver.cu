@@ -185,6 +185,14 @@ struct tafv_gpu {
   int ntile_k = 0;
   long long gcount[kMaxLevels] = {};  // owned counts over all ranks
   bool sharded() const { return comm != nullptr; }
+  // traversal direction of the next hot kernel (alternating, see k_grad_limit)
+  bool alt_dir = true;
+  int dir_state = 0;
+  int next_dir() {
+    if (!alt_dir) return 0;
+    dir_state ^= 1;
+    return dir_state;
+  }
 
   // stats
   int64_t launches = 0;
@@ -991,16 +999,17 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
   timed(h, tafv_gpu::kK1, [&] {
-    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, front, pred ? 1 : 0);
+    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, front, pred ? 1 : 0, h.next_dir());
   }, na, nf, nfr);
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
-    if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan);
-    else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan);
+    const int r2 = h.next_dir();
+    if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan, r2);
+    else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan, r2);
   }, na, nf, nfr);
   if (last) {
     timed(h, tafv_gpu::kK3C, [&] {
       k_gather_update<P, false, true, DEG><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, ncp,
-                                                                          h.dplan, h.partials);
+                                                                          h.dplan, h.partials, 0);
     }, na, nf, 0);
     k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan);
     h.launches += 4;
@@ -1011,10 +1020,11 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     halo_rows(h, h.w, P::NV);  // the next iteration stages the halo's new w
   } else {
     timed(h, pred ? tafv_gpu::kK3P : tafv_gpu::kK3C, [&] {
+      const int r3 = h.next_dir();
       if (pred)
-        k_gather_update<P, true, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials);
+        k_gather_update<P, true, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials, r3);
       else
-        k_gather_update<P, false, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials);
+        k_gather_update<P, false, false, DEG><<<g3, 128, 0, h.st>>>(md, sd, cl, ncp, h.dplan, h.partials, r3);
     }, na, nf, 0);
     h.launches += 3;
     // shards: the just-updated rows of owned cells to the peers' halos
@@ -1042,6 +1052,7 @@ void sweep(tafv_gpu& h) {
 }
 
 void enqueue_sweep_direct(tafv_gpu& h) {
+  h.dir_state = 1;  // the sweep's first kernel walks forwards (fixed per graph)
   CK(cudaMemsetAsync(&h.dplan->nonfinite, 0, sizeof(int), h.st));
   switch (h.model) {
     case TAFV_ADVECTION: sweep<Advection2D>(h); break;
@@ -1563,6 +1574,13 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
     } else if (n == "slot_geo") {
       h->slot_geo = value != 0;
+      for (auto& g : h->graphs) {
+        cudaGraphExecDestroy(g.second.exec);
+        for (auto e : g.second.evs) cudaEventDestroy(e);
+      }
+      h->graphs.clear();
+    } else if (n == "alt_dir") {
+      h->alt_dir = value != 0;
       for (auto& g : h->graphs) {
         cudaGraphExecDestroy(g.second.exec);
         for (auto e : g.second.evs) cudaEventDestroy(e);
