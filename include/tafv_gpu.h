@@ -232,6 +232,28 @@ int tafv_gpu_create_shard(const tafv_mesh_view* global_mesh, const tafv_physics*
                           const int32_t* rank_of_cell, int32_t rank, tafv_comm* comm,
                           tafv_gpu** out);
 
+/* ---- formats (host only) ----------------------------
+ * TFVM mesh files: version 1 = the reference's 2D format (Mesh::save,
+ * mesh.cpp:345-382), read here; version 2 = Vec3 geometry + connectivity,
+ * written here. Two-call load: NULL arrays -> counts only. */
+int tafv_mesh_save(const char* path, const tafv_mesh_view* mesh);
+int tafv_mesh_load(const char* path, int32_t* dim, int32_t* n_cells, int32_t* n_faces,
+                   double* cell_volume, double* cell_centroid, double* cell_char_length,
+                   int32_t* face_left, int32_t* face_right, int32_t* face_partner, double* face_normal,
+                   double* face_area, double* face_centroid);
+/* Mesh::hash (mesh.cpp:326-343, FNV-1a): identical for dim <= 2; + z in 3D. */
+uint64_t tafv_mesh_hash(const tafv_mesh_view* mesh);
+/* Snapshots (save_snapshot / Snapshot::load, state.cpp:77-116): text
+ * "tafv-snapshot 1" byte-identical to the reference for nv == 1, "... 2" with
+ * a component count for nv > 1, or binary TFVS (binary != 0). Rows [n][nv]. */
+int tafv_snapshot_save(const char* path, int32_t binary, uint64_t mesh_hash, int32_t n_cells, int32_t nv,
+                       double time, int32_t iteration, const double* w, const double* W);
+int tafv_snapshot_load(const char* path, uint64_t* mesh_hash, int32_t* n_cells, int32_t* nv, double* time,
+                       int32_t* iteration, double* w, double* W);
+/* compare_snapshots (state.cpp:118-132): max relative difference over w, W. */
+int tafv_snapshot_compare(const char* path_a, const char* path_b, double* worst);
+const char* tafv_io_last_error(void);
+
 /* 3D hexahedral mesh generator (new: the reference generator is 1D/2D only,
  * mesh.cpp:302-317). Tensor-product node lattice x[nx+1], y[ny+1], z[nz+1],
  * interior nodes jittered uniformly by +-jitter of the local spacing

@@ -96,6 +96,9 @@ def _load(path, kind):
     getattr(lib, p + "minmod").argtypes = [C.c_double, C.c_double]
     if kind == "ref":
         lib.ref_mesh_hash.restype = C.c_uint64
+        lib.ref_mesh_save.argtypes = [C.c_void_p, C.c_char_p]
+        lib.ref_snapshot_save.argtypes = [C.c_void_p, C.c_char_p]
+        lib.ref_snapshot_compare.argtypes = [C.c_char_p, C.c_char_p, C.c_void_p]
         lib.ref_total_extensive.restype = C.c_double
         lib.ref_total_extensive.argtypes = [C.c_void_p]
     _LIBS[path] = lib

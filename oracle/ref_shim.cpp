@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <fstream>
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
@@ -155,6 +156,15 @@ void ref_mesh_counts(void* mp, int* nc, int* nf, int* nadj) {
 
 uint64_t ref_mesh_hash(void* mp) { return static_cast<Mesh*>(mp)->hash(); }
 
+// Mesh::save (mesh.cpp:345-382) to a file.
+int ref_mesh_save(void* mp, const char* path) {
+  return guard([&] {
+    std::ofstream os(path, std::ios::binary);
+    static_cast<Mesh*>(mp)->save(os);
+    if (!os) throw std::runtime_error("ref_mesh_save: write failed");
+  });
+}
+
 // cell: nc x 4 (cx, cy, volume, char_length); face_i: nf x 3 (left, right,
 // partner); face_d: nf x 5 (nx, ny, area, fcx, fcy).
 void ref_mesh_export(void* mp, double* cell, int* face_i, double* face_d, int* adj_off,
@@ -263,6 +273,23 @@ void ref_time(void* sp, double* t0, int* iteration) {
   auto* s = static_cast<Solver*>(sp);
   *t0 = s->st.t0;
   *iteration = s->st.iteration;
+}
+
+// save_snapshot (state.cpp:77-91) to a file.
+int ref_snapshot_save(void* sp, const char* path) {
+  return guard([&] {
+    auto* s = static_cast<Solver*>(sp);
+    std::ofstream os(path);
+    save_snapshot(os, *s->mesh, s->st);
+  });
+}
+
+// compare_snapshots(Snapshot::load(a), Snapshot::load(b)) (state.cpp:93-132).
+int ref_snapshot_compare(const char* a, const char* b, double* worst) {
+  return guard([&] {
+    std::ifstream ia(a), ib(b);
+    *worst = compare_snapshots(Snapshot::load(ia), Snapshot::load(ib));
+  });
 }
 
 double ref_total_extensive(void* sp) { return static_cast<Solver*>(sp)->st.total_extensive(); }

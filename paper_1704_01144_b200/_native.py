@@ -108,6 +108,8 @@ EXPORTS = [
     "tafv_partition_slabs", "tafv_shard_describe", "tafv_shard_last_error",
     "tafv_comm_nccl_unique_id", "tafv_comm_create_nccl", "tafv_comm_create_loopback",
     "tafv_comm_destroy", "tafv_gpu_create_shard",
+    "tafv_mesh_save", "tafv_mesh_load", "tafv_mesh_hash", "tafv_snapshot_save", "tafv_snapshot_load",
+    "tafv_snapshot_compare", "tafv_io_last_error",
 ]
 
 _lib = None
@@ -151,5 +153,14 @@ def lib():
     L.tafv_comm_destroy.restype = None
     L.tafv_gpu_create_shard.argtypes = [C.POINTER(MeshView), C.POINTER(Physics), C.c_int, vp, i32, vp,
                                         C.POINTER(vp)]
+    L.tafv_mesh_save.argtypes = [C.c_char_p, C.POINTER(MeshView)]
+    L.tafv_mesh_load.argtypes = [C.c_char_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    L.tafv_mesh_hash.argtypes = [C.POINTER(MeshView)]
+    L.tafv_mesh_hash.restype = C.c_uint64
+    L.tafv_snapshot_save.argtypes = [C.c_char_p, i32, C.c_uint64, i32, i32, dbl, i32, vp, vp]
+    L.tafv_snapshot_load.argtypes = [C.c_char_p, C.POINTER(C.c_uint64), C.POINTER(i32), C.POINTER(i32),
+                                     C.POINTER(dbl), C.POINTER(i32), vp, vp]
+    L.tafv_snapshot_compare.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(dbl)]
+    L.tafv_io_last_error.restype = C.c_char_p
     _lib = L
     return L
