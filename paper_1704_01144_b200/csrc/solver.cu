@@ -17,6 +17,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -41,6 +42,13 @@ using namespace tafv;
 namespace {
 
 thread_local std::string g_create_error;
+
+// NVTX ranges mirroring the reference's TraceRecord kinds (runtime.hpp:110-118):
+// one per plan, sweep and (direct launches) phase; free without a tool.
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 struct Error {
   int code;
@@ -852,6 +860,7 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt);
 // plan_iteration on the device: either the captured plan graph of these
 // options (kernels + the read-back copy, one launch) or direct launches.
 void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
+  const Range r("tafv.plan");
   require(opt.theta_max >= 0, "classify: theta_max must be >= 0");
   require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
   require(h.state_set, "plan: state not set");
@@ -1035,6 +1044,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
 
 template <class P>
 void phase(tafv_gpu& h, bool pred, bool last, int level, int front) {
+  const Range r(pred ? "tafv.phase.predictor" : (last ? "tafv.phase.trailing" : "tafv.phase.corrector"));
   if (h.deg6) phase_t<P, 6>(h, pred, last, level, front);
   else phase_t<P, 0>(h, pred, last, level, front);
 }
@@ -1066,6 +1076,7 @@ void enqueue_sweep_direct(tafv_gpu& h) {
 // launch reads its active count and dt from the device plan, so the graph
 // captured once replays for every later iteration with the same theta.
 void run_sweep(tafv_gpu& h) {
+  const Range r(h.sharded() ? "tafv.sweep.shard" : "tafv.sweep");
   if (!h.use_graph || (h.sharded() && !h.comm->capturable())) {
     enqueue_sweep_direct(h);
     return;
@@ -1560,7 +1571,11 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
       std::vector<int8_t> v(h->N);
       CK(cudaMemcpy(v.data(), n == "tau" ? h->tau : h->raw, h->N, cudaMemcpyDeviceToHost));
       int32_t* o = static_cast<int32_t*>(out);
-      for (int i = 0; i < h->N; ++i) o[h->cperm[i]] = v[i];
+      // shards: OWNED entries into the global array (like get_state)
+      for (int i = 0; i < h->N; ++i) {
+        if (h->sharded() && i >= h->n_own) continue;
+        o[h->sharded() ? h->shard_cells[h->cperm[i]] : h->cperm[i]] = v[i];
+      }
     } else {
       require(false, "get_array: unknown array");
     }

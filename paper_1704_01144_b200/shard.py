@@ -84,3 +84,11 @@ def local_mesh(mesh, sh):
         "fp": np.full(len(faces), -1, dtype=np.int32), "fn": mesh["fn"][faces], "fa": mesh["fa"][faces],
         "fc": mesh["fc"][faces],
     }
+
+
+def level_cost_weights(tau, theta=None):
+    """DistDriver::repartition weights 2^(theta - tau) (exchange.cpp:598-603)."""
+    import numpy as _np
+    tau = _np.asarray(tau)
+    th = int(tau.max()) if theta is None else int(theta)
+    return _np.ldexp(1.0, th - tau)

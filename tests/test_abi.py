@@ -134,3 +134,17 @@ def test_config_sizes_match_baseline():
     assert configs.get(3).n_cells == 8_000_000
     assert configs.get(4).n_cells == 80_062_991
     assert configs.get(5).n_cells == 16_003_008
+
+
+def test_observe_tables_and_csv(tmp_path):
+    """Paper Table 1 shares through the observability helpers."""
+    from paper_1704_01144_b200 import observe
+    rec = {"theta": 2, "level_cells": [5, 242, 9753], "cost_ratio": 3.9, "iteration": 1, "t_start": 0.0,
+           "dt": 0.1, "advance": 0.4, "total_extensive": [1.0, 2.0]}
+    tab = observe.level_table(rec)
+    for got, want in zip([x[3] for x in tab], [0.20, 4.72, 95.08]):  # PAPER.md:570-583, test_levels.cpp:69-77
+        assert abs(got - want) <= 0.01
+    p = tmp_path / "r.csv"
+    observe.records_to_csv([rec, rec], p, kernel_times={"K1": {"ms": 1.0, "launches": 2}})
+    lines = p.read_text().splitlines()
+    assert lines[0].startswith("iteration,t_start,dt,theta") and len(lines) >= 3

@@ -326,3 +326,64 @@ def test_nccl_single_rank_shard(gpu):
     s.close()
     comm.close()
     del shard
+
+
+def test_sharded_repartition_by_level_cost_bitwise(gpu):
+    """DistDriver::repartition (exchange.cpp:595-609) on the GPU path: run,
+    re-cut the slabs by level cost 2^(theta - tau), continue; the state is
+    bitwise identical to an undisturbed single-domain run."""
+    import threading
+
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    cfg = configs.get(3, 10)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    world, n1, n2 = 2, 2, 2
+    roc = shard.partition_slabs(mesh, world, axis=0)
+    comm = Comm.loopback(world)
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(world)]
+    bar = threading.Barrier(world)
+    parts, errs, out = {}, [], {}
+    state = {}
+
+    def body(r):
+        try:
+            s = solvers[r]
+            s.set_state(w0)
+            s.reference_integrate(cfg.options(), n1)
+            w, W, t0, it = s.get_state()
+            parts[r] = (w, W, s.get_array("tau"), t0, it)
+            bar.wait()
+            if r == 0:  # assemble the global state and the new cut
+                state["w"] = sum(parts[q][0] for q in range(world))
+                state["W"] = sum(parts[q][1] for q in range(world))
+                tau = sum(parts[q][2] for q in range(world))
+                state["roc"] = shard.partition_slabs(mesh, world, axis=0,
+                                                     weight=shard.level_cost_weights(tau))
+            bar.wait()
+            s.close()
+            bar.wait()
+            s2 = Solver(mesh, "euler", shard=(state["roc"], r, comm))
+            s2.set_state(state["w"], state["W"], parts[r][3], parts[r][4])
+            s2.reference_integrate(cfg.options(), n2)
+            out[r] = s2.get_state()
+            s2.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+            bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    comm.close()
+    assert not errs, errs
+    assert not np.array_equal(state["roc"], roc)  # the cut moved
+    w = sum(out[r][0] * (state["roc"] == r)[:, None] for r in range(world))
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    g.reference_integrate(cfg.options(), n1 + n2)
+    np.testing.assert_array_equal(w, g.get_state()[0])
+    assert out[0][3] == n1 + n2
