@@ -159,6 +159,40 @@ def traffic_from_profiles(kind):
     return e.get("bytes_per_launch"), e.get("source")
 
 
+def reference_library_scalar2d(threads, iterations=2):
+    """The UNMODIFIED reference library (oracle/_ref, compiled from
+    proj/core) on its own scalar-2D workload with the same cell count as
+    config 2: 800x800 periodic torus with a 2x-refined centre block
+    (1.12M cells, 2 temporal levels), advection a=(1, 0.5), theta_max 3,
+    CFL 0.5. Times its sequential reference_integrate (reference.cpp:131-140)
+    and its task-parallel TaskEngine::integrate (taskgen.cpp:663-675, all host
+    threads). Context only: the reference has no Euler-3D model."""
+    try:
+        from oracle import RefSolver, ref_available, ref_generate_mesh
+        if not ref_available():
+            return {"unavailable": "oracle/_ref/libtafv_ref.so not built"}
+        _, _, mh = ref_generate_mesh(dim=2, nx=800, ny=800, periodic_x=True, periodic_y=True,
+                                     regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+        out = {"workload": "scalar 2D advection, 800x800 torus + 2x block (reference generate_mesh)",
+               "unit": UNIT}
+        for leg in ("sequential", "task_engine"):
+            s = RefSolver(mh, "advection", (1.0, 0.5))
+            s.init_gaussian(sigma=0.15)
+            s.set_options(3, 0.5, 1.0)
+            run = (lambda n: s.integrate(n)) if leg == "sequential" else \
+                (lambda n: s.task_integrate(n, threads, 4 * threads))
+            run(1)
+            t = time.perf_counter()
+            recs = run(iterations)
+            dt = time.perf_counter() - t
+            out["cells"] = s.nc
+            out[leg] = {"value": sum(c_eff(r) for r in recs) / dt, "iterations": iterations, "seconds": dt,
+                        "cores": 1 if leg == "sequential" else threads}
+        return out
+    except Exception as e:  # context field only; never fails the arm
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle port (all host threads), rank 0 only."""
     if rank != 0:
@@ -189,6 +223,7 @@ def run_reference(args, rank, world):
                                    "warm-up, oracle/tafv_oracle.cpp Euler port (the reference library "
                                    "proj/core is scalar-2D only and cannot run this config)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_library_scalar2d": reference_library_scalar2d(threads),
     }
     print(json.dumps(line), flush=True)
 

@@ -320,6 +320,14 @@ class RefSolver(_SolverBase):
     def total_extensive(self):
         return self.lib.ref_total_extensive(self.h)
 
+    def task_integrate(self, n, workers, ces):
+        """The reference's task-parallel path: TaskEngine::integrate
+        (taskgen.cpp:663-675) on `workers` single-lane workers, `ces`
+        computation elements, prio scheduler, task packing on."""
+        recs = (Record * max(1, n))()
+        self._c(self.lib.ref_taskengine_integrate(self.h, n, workers, ces, recs))
+        return [recs[i].as_dict() for i in range(n)]
+
 
 class OracleMesh:
     def __init__(self, mesh, closure_mask=None):

@@ -19,7 +19,11 @@
 #include <string>
 #include <vector>
 
+#include "tafv/ce.hpp"
 #include "tafv/kernels.hpp"
+#include "tafv/partition.hpp"
+#include "tafv/runtime.hpp"
+#include "tafv/taskgen.hpp"
 #include "tafv/levels.hpp"
 #include "tafv/mesh.hpp"
 #include "tafv/physics.hpp"
@@ -352,6 +356,30 @@ int ref_integrate(void* sp, int n, Record* recs) {
   return guard([&] {
     auto* s = static_cast<Solver*>(sp);
     const auto r = reference_integrate(*s->mesh, s->st, s->opt, n);
+    for (size_t i = 0; i < r.size(); ++i) fill(&recs[i], r[i]);
+  });
+}
+
+// The reference's own task-parallel CPU path (TaskEngine::integrate,
+// taskgen.cpp:663-675) over `workers` single-lane workers and `ces`
+// computation elements, prio scheduler, packing on (the survey's baseline
+// shape).
+int ref_taskengine_integrate(void* sp, int n, int workers, int ces, Record* recs) {
+  return guard([&] {
+    auto* s = static_cast<Solver*>(sp);
+    RuntimeOptions ro;
+    ro.worker_lanes.assign(workers, 1);
+    ro.scheduler = "prio";
+    ro.probe_period_ms = 0.0;
+    ro.record_trace = false;
+    Runtime rt(ro);
+    const Partition part =
+        make_partition(*s->mesh, 1, ces, std::vector<int64_t>(s->mesh->cell_count(), 1));
+    const CESet set = build_ces(*s->mesh, part);
+    TaskgenOptions topt;
+    topt.packing = true;
+    TaskEngine engine(*s->mesh, set, rt, topt);
+    const auto r = engine.integrate(s->st, s->opt, n);
     for (size_t i = 0; i < r.size(); ++i) fill(&recs[i], r[i]);
   });
 }

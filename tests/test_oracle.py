@@ -337,6 +337,29 @@ def test_integrate_vs_reference(spec, model, a, opts, n):
 
 
 @needs_ref
+@pytest.mark.parametrize("workers,ces", [(1, 1), (4, 16)])
+def test_reference_task_engine_equals_sequential_and_oracle(workers, ces):
+    """The reference's task-parallel CPU path (TaskEngine, the bench's
+    reference-library arm) produces the same iterations as its sequential
+    reference_integrate and as the oracle, bitwise (test_taskgen.cpp's
+    engine-vs-reference property)."""
+    spec = dict(dim=2, nx=40, ny=32, periodic_x=True, periodic_y=True, regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+    m, _, mh = ref_generate_mesh(**spec)
+    seq, task = RefSolver(mh, "advection", (1.0, 0.5)), RefSolver(mh, "advection", (1.0, 0.5))
+    for s in (seq, task):
+        s.init_gaussian(sigma=0.15)
+        s.set_options(3, 0.5, 1.0)
+    o = OracleSolver(m, "advection", (1.0, 0.5))
+    o.set_options(3, 0.5, 1.0)
+    o.init_values(seq.get("w"))
+    rs, rt, ro = seq.integrate(4), task.task_integrate(4, workers, ces), o.integrate(4)
+    assert [r["dt"] for r in rs] == [r["dt"] for r in rt] == [r["dt"] for r in ro]
+    assert [r["level_cells"] for r in rs] == [r["level_cells"] for r in rt]
+    assert np.array_equal(seq.get("w"), task.get("w"))
+    assert np.array_equal(seq.get("w"), o.get("w"))
+
+
+@needs_ref
 def test_theta0_equals_heun_vs_reference():  # test_numerics.cpp:490-525
     m, _, mh = ref_generate_mesh(dim=1, nx=8, periodic_x=True, regions=[((0.375, 0.0, 0.625, 1.0), 4)])
     o1 = OracleSolver(m, "advection", (1.0, 0.0))
