@@ -45,9 +45,10 @@ UNIT = "cell-updates/s"
 #   K1 per active cell: staged state 40, tau 1, CSR offset 4, 6 slots x 8,
 #      volume 8, centroid 24, gradient write 120;  per active face: normal+area
 #      32 + centroid 24;  per fringe cell: w and w_pred 80 + tau 1.
-#   K2 per active face: left/right 8, normal+area 32, centroid 24, cadence 1,
-#      pred: phi write 40 + window reset 40; corr: phi read 40 + window
-#      read/write 80 + substep write 40;  per touched cell (active + fringe):
+#   K2 per active face: left/right 8, normal+area 32, centroid 24,
+#      pred: phi write 40; corr: cadence 1, phi read 40, substep write 40,
+#      window-alias byte 1 (int_window traffic, 40-80 B, only on unequal-level
+#      faces: not counted, a lower bound);  per touched cell (active + fringe):
 #      state 40, gradient 120, centroid 24, tau 1 (fringe +40 for the 2nd state).
 #   K3 per active cell: tau 1, offset 4, 6 face ids x 4, volume 8, W 40,
 #      pred: w_pred write 40; corr: W + w writes 80;  per active face: flux 40
@@ -57,9 +58,9 @@ def kernel_bytes(kind, cells, faces, fringe, slots_per_cell):
     if kind == "K1_grad_limit":
         return cells * (40 + 1 + 4 + 8 * slot_b + 8 + 24 + 120) + faces * 56 + fringe * 81
     if kind == "K2_face_pred":
-        return faces * (8 + 32 + 24 + 80) + cells * 185 + fringe * 225
+        return faces * (8 + 32 + 24 + 40) + cells * 185 + fringe * 225
     if kind == "K2_face_corr":
-        return faces * (8 + 32 + 24 + 1 + 160) + cells * 185 + fringe * 225
+        return faces * (8 + 32 + 24 + 1 + 81) + cells * 185 + fringe * 225
     if kind == "K3_update_pred":
         return cells * (1 + 4 + 4 * slot_b + 8 + 40 + 40) + faces * 40
     if kind == "K3_update_corr":

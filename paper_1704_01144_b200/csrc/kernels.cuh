@@ -70,6 +70,13 @@ struct StateDev {
   double* phi;   // [F][NV] phi_pred
   double* isub;  // [F][NV] int_substep
   double* iwin;  // [F][NV] int_window
+  // [F] or null. Equal-level faces (both sides at the face's cadence, or a
+  // boundary face) open a window at every one of their substeps, so their
+  // int_window is always 0.0 + int_substep and no gather ever reads it (K3
+  // reads int_window only on the coarser side of a fringe face). With
+  // `ialias` set K2 skips those faces' window reset and accumulation and
+  // records alias = 1; get_array("int_window") materialises isub + 0.0.
+  uint8_t* ialias;
 };
 
 struct PlanDev {
@@ -313,8 +320,10 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
       }
     }
     bool shared_start = (front & ((1 << tl) - 1)) == 0;
+    bool eq = true;  // equal-level (or boundary) face
     if (lr.y >= 0) {
       const int tr = __ldg(s.tau + lr.y);
+      eq = tr == tl;
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
       double we[NV];
       stage<NV>(s, lr.y, tr, front, PRED, we);
@@ -339,20 +348,22 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     if (PRED) {
 #pragma unroll
       for (int k = 0; k < NV; ++k) phi[k] = r[k] * gm.w;
-      if (shared_start) {
+      if (shared_start && !(eq && s.ialias)) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) iwin[k] = 0.0;
       }
     } else {
       const double dt_sub = dt * (double)(1 << s.cad[f]);
       double* isub = s.isub + (size_t)f * NV;
+      const bool skip = eq && s.ialias;
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         const double phi_corr = r[k] * gm.w;
         const double v = 0.5 * dt_sub * (phi[k] + phi_corr);
         isub[k] = v;
-        iwin[k] = iwin[k] + v;
+        if (!skip) iwin[k] = iwin[k] + v;
       }
+      if (s.ialias) s.ialias[f] = skip ? 1 : 0;
     }
   }
 }
@@ -722,6 +733,17 @@ __global__ void k_gather_rows(const double* src, const int* perm, int n, int wid
     const size_t row = i / width, col = i % width;
     dst[i] = src[(size_t)perm[row] * width + col];
   }
+}
+
+// int_window with aliased (equal-level) faces materialised: isub + 0.0, the
+// value the reference's reset-then-accumulate leaves (kernels.cpp:123-130,
+// 183-185).
+__global__ void k_window_rows(const double* iwin, const double* isub, const uint8_t* alias, int n,
+                              int width, double* dst) {
+  const long long total = (long long)n * width;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    dst[i] = alias[i / width] ? isub[i] + 0.0 : iwin[i];
 }
 
 __global__ void k_scatter_rows(const double* src, const int* perm, int n, int width, double* dst) {

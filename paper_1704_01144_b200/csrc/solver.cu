@@ -141,6 +141,8 @@ struct tafv_gpu {
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
   double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
+  uint8_t* ialias = nullptr;  // [F] see StateDev::ialias
+  bool iwin_alias = true;
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
   uint8_t* fflag = nullptr;
   double *dtmax = nullptr, *blockmin = nullptr;
@@ -212,7 +214,9 @@ struct tafv_gpu {
                    periodic ? rcf : nullptr, geo, fcen, slot_geo ? sgeo : nullptr,
                    slot_geo ? sdx : nullptr};
   }
-  StateDev state_dev() const { return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin}; }
+  StateDev state_dev() const {
+    return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr};
+  }
 
   double* staging(size_t n) {
     if (n > stage_len) {
@@ -238,7 +242,7 @@ struct tafv_gpu {
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
     void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
-                    grad, phi,   isub,     iwin,     tau,    cad,    raw,      tmpa,    tmpb,
+                    grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
                     klist != clist ? klist : nullptr, k1_counts};
@@ -593,6 +597,8 @@ void alloc_state(tafv_gpu& h) {
   CK(cudaMemset(h.phi, 0, F * nv * sizeof(double)));
   CK(cudaMemset(h.isub, 0, F * nv * sizeof(double)));
   CK(cudaMemset(h.iwin, 0, F * nv * sizeof(double)));
+  h.ialias = dalloc<uint8_t>(F);
+  CK(cudaMemset(h.ialias, 0, F));
   h.tau = dalloc<int8_t>(N);
   h.raw = dalloc<int8_t>(N);
   h.tmpa = dalloc<int8_t>(N);
@@ -1566,7 +1572,13 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     else if (n == "dt_max") rows(h->dtmax, h->N, 1, h->d_cperm);
     else if (n == "phi_pred") rows(h->phi, h->F, h->nv, h->d_fperm);
     else if (n == "int_substep") rows(h->isub, h->F, h->nv, h->d_fperm);
-    else if (n == "int_window") rows(h->iwin, h->F, h->nv, h->d_fperm);
+    else if (n == "int_window") {
+      double* win = dalloc<double>((size_t)h->F * h->nv);
+      k_window_rows<<<h->grid_for((long long)h->F * h->nv, 256), 256, 0, h->st>>>(h->iwin, h->isub, h->ialias,
+                                                                             h->F, h->nv, win);
+      rows(win, h->F, h->nv, h->d_fperm);
+      cudaFree(win);
+    }
     else if (n == "raw_level" || n == "tau") {
       std::vector<int8_t> v(h->N);
       CK(cudaMemcpy(v.data(), n == "tau" ? h->tau : h->raw, h->N, cudaMemcpyDeviceToHost));
@@ -1594,8 +1606,8 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
         for (auto e : g.second.evs) cudaEventDestroy(e);
       }
       h->graphs.clear();
-    } else if (n == "alt_dir") {
-      h->alt_dir = value != 0;
+    } else if (n == "alt_dir" || n == "iwin_alias") {
+      (n == "alt_dir" ? h->alt_dir : h->iwin_alias) = value != 0;
       for (auto& g : h->graphs) {
         cudaGraphExecDestroy(g.second.exec);
         for (auto e : g.second.evs) cudaEventDestroy(e);

@@ -204,10 +204,12 @@ def test_divergence_detected(gpu):
         s.reference_integrate(cfg.options(), 3)
 
 
-@pytest.mark.parametrize("use_graph,slot_geo", [(0, 0), (1, 0), (0, 1), (1, 1)])
-def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, gpu):
-    """The CUDA-graph sweep and the direct-launch sweep both reproduce the
-    oracle bitwise (records included), through reference_integrate."""
+@pytest.mark.parametrize("use_graph,slot_geo,iwin_alias", [(0, 0, 1), (1, 0, 1), (0, 1, 1), (1, 1, 1),
+                                                            (1, 1, 0)])
+def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, iwin_alias, gpu):
+    """The CUDA-graph sweep and the direct-launch sweep, with and without
+    the int_window alias, reproduce the oracle bitwise (records included),
+    through reference_integrate."""
     from oracle import OracleSolver
     cfg = configs.get(2, 5)
     mesh = cfg.mesh()
@@ -216,6 +218,7 @@ def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, gpu):
     g = Solver(mesh, "euler")
     g.set_flag("use_graph", use_graph)
     g.set_flag("slot_geo", slot_geo)
+    g.set_flag("iwin_alias", iwin_alias)
     g.set_state(w0)
     rg = g.reference_integrate(opt, 6)
     o = OracleSolver(mesh, "euler", threads=8)
@@ -230,6 +233,25 @@ def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, gpu):
     assert [r["level_cells"] for r in rg] == [r["level_cells"] for r in ro]
     assert [r["iteration"] for r in rg] == [r["iteration"] for r in ro]
     assert [r["t_start"] for r in rg] == [r["t_start"] for r in ro]
+
+
+@pytest.mark.parametrize("cid,scale", [(2, 6), (4, 8)])
+def test_window_alias_is_invisible(cid, scale, gpu):
+    """Skipping int_window traffic on equal-level faces (StateDev::ialias)
+    changes nothing observable: state, int_substep, phi_pred and the
+    materialised int_window equal the full-traffic run bitwise."""
+    cfg = configs.get(cid, scale)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    out = []
+    for alias in (0, 1):
+        g = Solver(mesh, "euler")
+        g.set_flag("iwin_alias", alias)
+        g.set_state(w0)
+        g.reference_integrate(cfg.options(), 3)
+        out.append([g.get_state()[0]] + [g.get_array(k) for k in ("int_window", "int_substep", "phi_pred")])
+    for a, b in zip(*out):
+        assert a.tobytes() == b.tobytes()
 
 
 def test_cpp_shim_caller(gpu):
