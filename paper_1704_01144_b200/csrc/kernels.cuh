@@ -99,26 +99,30 @@ struct PlanDev {
 // (kernels.cpp:31-63): at `front`, a cell whose window boundary lies on the
 // front (offset 0) stages w (predictor) or w_pred (corrector); a fringe cell
 // straddling the front stages w + theta_f (w_pred - w), theta_f = offset/2^tau.
+// The row an offset-0 cell stages (w in a predictor, w_pred in a corrector)
+// is loaded together with tau, so the common case costs one dependent load,
+// not two; a cell straddling the front then loads its other row and
+// interpolates. Returns tau.
 template <int NV>
-__device__ __forceinline__ void stage(const StateDev& s, int x, int tx, int front, bool pred,
-                                      double* out) {
+__device__ __forceinline__ int stage_spec(const StateDev& s, int x, int front, bool pred, double* out) {
+  const double* base = (pred ? s.w : s.wp) + (size_t)x * NV;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = __ldg(base + k);
+  const int tx = __ldg(s.tau + x);
   const int win = 1 << tx;
   const int off = front & (win - 1);
-  // read-only within K1/K2 (only K3 writes w / w_pred): non-coherent path
-  const double* w = s.w + (size_t)x * NV;
-  const double* wp = s.wp + (size_t)x * NV;
-  if (off == 0) {
-    const double* src = pred ? w : wp;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) out[k] = __ldg(src + k);
-  } else {
+  if (off != 0) {
     const double th = (double)off / (double)win;
+    const double* other = (pred ? s.wp : s.w) + (size_t)x * NV;
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const double a = __ldg(w + k);
-      out[k] = a + th * (__ldg(wp + k) - a);
+      const double o = __ldg(other + k);
+      const double a = pred ? out[k] : o;   // w
+      const double b = pred ? o : out[k];   // w_pred
+      out[k] = a + th * (b - a);
     }
   }
+  return tx;
 }
 
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
     const int i = rev ? n - 1 - ii : ii;
     const int c = list ? list[i] : i;
     double we[NV];
-    stage<NV>(s, c, __ldg(s.tau + c), front, pred, we);
+    stage_spec<NV>(s, c, front, pred, we);
     double g[NV][D];
     double wmin[NV], wmax[NV];
 #pragma unroll
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #ifdef TAFV_EXP_NO_GATHER
         for (int k = 0; k < NV; ++k) wn[k] = we[k] * (1.0 + 1e-3 * t);  // timing experiment only
 #else
-        stage<NV>(s, nb, __ldg(s.tau + nb), front, pred, wn);
+        stage_spec<NV>(s, nb, front, pred, wn);
 #endif
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -305,11 +309,11 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     const double4 gm = m.geo[f];
     const double nrm[3] = {gm.x, gm.y, gm.z};
     const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
-    const int tl = __ldg(s.tau + lr.x);
     double wL[NV], wR[NV];
+    int tl;
     {
       double we[NV];
-      stage<NV>(s, lr.x, tl, front, PRED, we);
+      tl = stage_spec<NV>(s, lr.x, front, PRED, we);
       const double* g = s.grad + (size_t)lr.x * NV * 3;
       const double cl[3] = {m.cen[3 * (size_t)lr.x], m.cen[3 * (size_t)lr.x + 1], m.cen[3 * (size_t)lr.x + 2]};
 #pragma unroll
@@ -322,11 +326,10 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     bool shared_start = (front & ((1 << tl) - 1)) == 0;
     bool eq = true;  // equal-level (or boundary) face
     if (lr.y >= 0) {
-      const int tr = __ldg(s.tau + lr.y);
+      double we[NV];
+      const int tr = stage_spec<NV>(s, lr.y, front, PRED, we);
       eq = tr == tl;
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
-      double we[NV];
-      stage<NV>(s, lr.y, tr, front, PRED, we);
       const double* g = s.grad + (size_t)lr.y * NV * 3;
       const double cr[3] = {m.cen[3 * (size_t)lr.y], m.cen[3 * (size_t)lr.y + 1], m.cen[3 * (size_t)lr.y + 2]};
       const double* to = m.fcen + 3 * (size_t)(m.rcf ? m.rcf[f] : f);
