@@ -484,14 +484,19 @@ __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks,
 
 // ---- plan kernels ----------------------------------------------------------
 // kernels.cpp:247-254: dt_max = speed > 0 ? min(dt_cap, cfl*h/speed) : dt_cap,
-// then the order-free min of kernels.cpp:260-264 as per-block partials.
-// With tau != null (synthetic level maps) the bound is dt_max / 2^tau.
+// and the order-free minimum of kernels.cpp:260-264 in the SAME launch: each
+// block leaves its minimum, the last block to finish (fence + ticket) reduces
+// them into plan->dt_min. With tau != null (synthetic level maps) the bound is
+// dt_max / 2^tau. `reset` (plan_iteration): that block also clears the plan's
+// error flag and counts for the counting kernels that follow.
 template <class P>
 __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParams pp, double cfl,
                                                 double dt_cap, double* dt_max, double* block_min,
-                                                const int8_t* tau_scale, int n) {
+                                                const int8_t* tau_scale, int n, unsigned* ticket,
+                                                PlanDev* plan, int reset) {
   constexpr int NV = P::NV;
-  double lowest = __longlong_as_double(0x7ff0000000000000ll);
+  constexpr double INF = __builtin_huge_val();
+  double lowest = INF;
   const int stride = gridDim.x * blockDim.x;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     double w[NV];
@@ -504,26 +509,37 @@ __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParam
     lowest = smin(lowest, b);
   }
   __shared__ double red[256];
-  red[threadIdx.x] = lowest;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
+  __shared__ bool last;
+  auto block_reduce = [&](double v) {
+    red[threadIdx.x] = v;
     __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    return red[0];
+  };
+  const double bm = block_reduce(lowest);
+  if (threadIdx.x == 0) {
+    block_min[blockIdx.x] = bm;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-  if (threadIdx.x == 0) block_min[blockIdx.x] = red[0];
-}
-
-__global__ void k_dt_min(const double* block_min, int nblocks, PlanDev* plan) {
-  __shared__ double red[256];
-  double lowest = __longlong_as_double(0x7ff0000000000000ll);
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) lowest = smin(lowest, block_min[b]);
-  red[threadIdx.x] = lowest;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
-    __syncthreads();
+  if (!last) return;
+  __threadfence();
+  lowest = INF;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+    lowest = smin(lowest, *((volatile const double*)block_min + b));
+  __syncthreads();
+  const double dmin = block_reduce(lowest);
+  if (threadIdx.x == 0) {
+    plan->dt_min = dmin;
+    *ticket = 0u;
+    if (reset) plan->err = 0;
   }
-  if (threadIdx.x == 0) plan->dt_min = red[0];
+  if (reset)
+    for (int i = threadIdx.x; i < 3 * kMaxLevels; i += blockDim.x) (&plan->cell_count[0])[i] = 0;
 }
 
 // levels.cpp:18-25: raw = ratio >= 1 ? ilogb(ratio) : 0, clamped.
@@ -564,13 +580,84 @@ __global__ void k_smooth(MeshDev m, const int8_t* in, int8_t* out, int n) {
   }
 }
 
+// Stable per-key compaction. Tile t covers items [t*kTile, (t+1)*kTile); the
+// count and scatter passes use the same tiling, so the order inside each key
+// bucket is ascending item id.
+constexpr int kTile = 2048;
+constexpr int kCompactThreads = 256;
+
+// Single-domain plan: classification (levels.cpp:18-25) fused into the first
+// Jacobi sweep (levels.cpp:33-46) -- a cell's and each neighbour's raw level
+// are classified on the fly from dt_max (the same quotient and exponent every
+// time), so no raw array is written -- and the per-tile level counts of the
+// compaction fused into the last sweep. FIRST: classify the inputs; SMOOTH
+// (theta_max > 0): apply the sweep, else the classification is the level;
+// COUNT: block b covers tile b and leaves its counts. clear_flag: the fringe
+// flags of the cells swept are cleared for k_face_cadence.
+template <bool FIRST, bool COUNT>
+__global__ void __launch_bounds__(kCompactThreads) k_level_sweep(MeshDev m, const int8_t* in,
+                                                                 const double* dt_max, const PlanDev* plan,
+                                                                 int theta_max, int smooth, int8_t* out,
+                                                                 int n, int nkeys, int* counts,
+                                                                 uint8_t* clear_flag) {
+  double dt_min = 0.0;
+  bool ok = false;
+  if (FIRST) {
+    dt_min = plan->dt_min;
+    ok = dt_min > 0.0 && isfinite(dt_min);
+  }
+  auto lev = [&](int x) -> int {
+    if (FIRST) return ok ? classify_raw(dt_max[x], dt_min, theta_max) : 0;
+    return in[x];
+  };
+  __shared__ int cnt[kMaxLevels];
+  if (COUNT) {
+    if (threadIdx.x < kMaxLevels) cnt[threadIdx.x] = 0;
+    __syncthreads();
+  }
+  const int beg = COUNT ? blockIdx.x * kTile + threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
+  const int end = COUNT ? min(n, (int)(blockIdx.x + 1) * kTile) : n;
+  const int step = COUNT ? blockDim.x : gridDim.x * blockDim.x;
+  for (int c = beg; c < end; c += step) {
+    int bound = lev(c);
+    if (smooth) {
+      const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
+      for (int t = s0; t < s1; ++t) {
+        const int nb = m.adj_nb[t];
+        if (nb >= 0) {
+          const int v = lev(nb) + 1;
+          bound = v < bound ? v : bound;
+        }
+      }
+    }
+    out[c] = (int8_t)bound;
+    if (clear_flag) clear_flag[c] = 0;
+    if (COUNT) atomicAdd(&cnt[bound], 1);
+  }
+  if (COUNT) {
+    __syncthreads();
+    if (threadIdx.x < nkeys) counts[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = cnt[threadIdx.x];
+  }
+}
+
 // levels.cpp:128-137 face cadence = min(tau_left, tau_right) (boundary: left),
-// plus the fringe flag of levels.cpp:139-153 (the coarser side of a face whose
-// sides differ) and the |dtau| <= 1 invariant the staging relies on.
-__global__ void k_face_cadence(MeshDev m, const int8_t* tau, int8_t* cad, uint8_t* fringe_flag,
-                               PlanDev* plan) {
-  const int stride = gridDim.x * blockDim.x;
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < m.n_faces; f += stride) {
+// the fringe flag of levels.cpp:139-153 (the coarser side of a face whose
+// sides differ; counted once per owned cell, by the face that sets it) and
+// the |dtau| <= 1 invariant the staging relies on, fused with the per-tile
+// cadence counts of the face compaction (faces [0, n_count)). Block b covers
+// face tile b.
+__global__ void __launch_bounds__(kCompactThreads) k_face_cadence(MeshDev m, const int8_t* tau, int8_t* cad,
+                                                                  unsigned* fflag32, PlanDev* plan, int n_own,
+                                                                  int n_count, int nkeys, int* counts,
+                                                                  int ntiles_count) {
+  __shared__ int cnt[kMaxLevels], fcnt[kMaxLevels];
+  if (threadIdx.x < kMaxLevels) {
+    cnt[threadIdx.x] = 0;
+    fcnt[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const int beg = blockIdx.x * kTile, end = min(m.n_faces, beg + kTile);
+  for (int f = beg + threadIdx.x; f < end; f += blockDim.x) {
     const int2 lr = m.lr[f];
     const int tl = tau[lr.x];
     int c = tl;
@@ -578,54 +665,67 @@ __global__ void k_face_cadence(MeshDev m, const int8_t* tau, int8_t* cad, uint8_
       const int tr = tau[lr.y];
       c = tl < tr ? tl : tr;
       if (tl != tr) {
-        fringe_flag[tl > tr ? lr.x : lr.y] = 1;
+        const int x = tl > tr ? lr.x : lr.y;
+        const int kx = tl > tr ? tl : tr;
+        const unsigned bit = 1u << (8 * (x & 3));
+        const unsigned old = atomicOr(&fflag32[x >> 2], bit);
+        if (!(old & bit) && x < n_own) atomicAdd(&fcnt[kx - 1], 1);
         const int d = tl > tr ? tl - tr : tr - tl;
         if (d > 1) atomicOr(&plan->err, 1);
       }
     }
     cad[f] = (int8_t)c;
-  }
-}
-
-// Stable per-key compaction. Tile t covers items [t*kTile, (t+1)*kTile); the
-// count and scatter passes use the same tiling, so the order inside each key
-// bucket is ascending item id.
-constexpr int kTile = 2048;
-constexpr int kCompactThreads = 256;
-
-__global__ void __launch_bounds__(kCompactThreads) k_tile_count(const int8_t* key, int n, int nkeys,
-                                                                int* counts /*[nkeys][ntiles]*/,
-                                                                const uint8_t* fringe_flag,
-                                                                PlanDev* plan) {
-  __shared__ int cnt[kMaxLevels];
-  __shared__ int fcnt[kMaxLevels];
-  if (threadIdx.x < kMaxLevels) {
-    cnt[threadIdx.x] = 0;
-    fcnt[threadIdx.x] = 0;
-  }
-  __syncthreads();
-  const int base = blockIdx.x * kTile;
-  for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
-    const int i = base + j;
-    if (i < n) {
-      const int k = key[i];
-      atomicAdd(&cnt[k], 1);
-      if (fringe_flag && fringe_flag[i] && k > 0) atomicAdd(&fcnt[k - 1], 1);
-    }
+    if (f < n_count) atomicAdd(&cnt[c], 1);
   }
   __syncthreads();
   if (threadIdx.x < nkeys) {
-    counts[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = cnt[threadIdx.x];
-    if (fringe_flag && fcnt[threadIdx.x])
+    if ((int)blockIdx.x < ntiles_count)
+      counts[(size_t)threadIdx.x * ntiles_count + blockIdx.x] = cnt[threadIdx.x];
+    if (fcnt[threadIdx.x])
       atomicAdd(reinterpret_cast<unsigned long long*>(&plan->fringe_count[threadIdx.x]),
                 (unsigned long long)fcnt[threadIdx.x]);
   }
 }
 
-// Exclusive scan over counts in (key, tile) order, in place; totals per key
-// into plan->cell_count or face_count. One block.
-__global__ void __launch_bounds__(1024) k_tile_scan(int* counts, int ntiles, int nkeys,
-                                                    long long* totals) {
+// Per-tile counts of keys (cells of an injected map; shard K1 list).
+__global__ void __launch_bounds__(kCompactThreads) k_tile_count(const int8_t* key, int n, int nkeys,
+                                                                int* counts /*[nkeys][ntiles]*/) {
+  __shared__ int cnt[kMaxLevels];
+  if (threadIdx.x < kMaxLevels) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int base = blockIdx.x * kTile;
+  for (int j = threadIdx.x; j < kTile; j += blockDim.x) {
+    const int i = base + j;
+    if (i < n) atomicAdd(&cnt[key[i]], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < nkeys) counts[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// One compaction (keys, per-tile counts, list, per-key totals, prefix sums of
+// the totals = active-set sizes of each level).
+struct CompactJob {
+  const int8_t* key;
+  int n, ntiles;
+  int* counts;       // [nkeys][ntiles]: counts in, exclusive offsets out
+  int* list;
+  long long* totals; // [kMaxLevels]
+  int* prefix;       // [kMaxLevels]
+};
+struct CompactJobs {
+  CompactJob j[3];
+  int njobs;
+};
+
+// Exclusive scan of each job's counts in (key, tile) order, in place; block b
+// scans job b, writes its per-key totals and their prefix sums. Block 0 (the
+// K3 cell list) also publishes the record counts and, for a single domain,
+// aliases the K1 list to it.
+__global__ void __launch_bounds__(1024) k_tile_scan(CompactJobs jobs, int nkeys, PlanDev* plan,
+                                                    int alias_k1) {
+  const CompactJob jb = jobs.j[blockIdx.x];
+  int* counts = jb.counts;
+  const int ntiles = jb.ntiles;
   const int total = ntiles * nkeys;
   const int per = (total + blockDim.x - 1) / blockDim.x;
   const int b = threadIdx.x * per, e = min(total, b + per);
@@ -649,34 +749,57 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int* counts, int ntiles, int
   __syncthreads();
   // per-key totals: next key's first offset minus this key's first offset
   if (threadIdx.x < nkeys) {
-    const int first = counts[(size_t)threadIdx.x * ntiles];
-    const int next = threadIdx.x + 1 < nkeys ? counts[(size_t)(threadIdx.x + 1) * ntiles] : part[blockDim.x - 1];
-    totals[threadIdx.x] = next - first;
+    long long t = 0;
+    if (ntiles > 0) {
+      const int first = counts[(size_t)threadIdx.x * ntiles];
+      const int next = threadIdx.x + 1 < nkeys ? counts[(size_t)(threadIdx.x + 1) * ntiles] : part[blockDim.x - 1];
+      t = next - first;
+    }
+    jb.totals[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long acc = 0;
+    for (int l = 0; l < kMaxLevels; ++l) {
+      const long long t = l < nkeys ? jb.totals[l] : 0;
+      acc += t;
+      jb.prefix[l] = (int)acc;
+      if (blockIdx.x == 0) {
+        plan->gcell_count[l] = t;
+        if (alias_k1) {
+          plan->k1_count[l] = t;
+          plan->nk1_prefix[l] = (int)acc;
+        }
+      }
+    }
   }
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(const int8_t* key, int n, int nkeys,
-                                                                  const int* offsets, int* list) {
+// Scatter of every job in one launch: blocks [0, ntiles_0) job 0, then job 1, ...
+__global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(CompactJobs jobs, int nkeys) {
   __shared__ int wcount[kCompactThreads / 32][kMaxLevels];
   __shared__ int running[kMaxLevels];
+  int tile = blockIdx.x, q = 0;
+  while (q + 1 < jobs.njobs && tile >= jobs.j[q].ntiles) tile -= jobs.j[q++].ntiles;
+  const CompactJob jb = jobs.j[q];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < nkeys) running[threadIdx.x] = offsets[(size_t)threadIdx.x * gridDim.x + blockIdx.x];
-  const int base = blockIdx.x * kTile;
+  if (threadIdx.x < nkeys) running[threadIdx.x] = jb.counts[(size_t)threadIdx.x * jb.ntiles + tile];
+  const int base = tile * kTile;
   const unsigned lt = (1u << lane) - 1u;
   for (int r = 0; r < kTile; r += blockDim.x) {
     const int i = base + r + threadIdx.x;
-    const int k = i < n ? key[i] : -1;
+    const int k = i < jb.n ? jb.key[i] : -1;
     int rank = 0;
-    for (int q = 0; q < nkeys; ++q) {
-      const unsigned mask = __ballot_sync(0xffffffffu, k == q);
-      if (k == q) rank = __popc(mask & lt);
-      if (lane == 0) wcount[warp][q] = __popc(mask);
+    for (int kk = 0; kk < nkeys; ++kk) {
+      const unsigned mask = __ballot_sync(0xffffffffu, k == kk);
+      if (k == kk) rank = __popc(mask & lt);
+      if (lane == 0) wcount[warp][kk] = __popc(mask);
     }
     __syncthreads();
     if (k >= 0) {
       int pos = running[k] + rank;
       for (int w = 0; w < warp; ++w) pos += wcount[w][k];
-      list[pos] = i;
+      jb.list[pos] = i;
     }
     __syncthreads();
     if (threadIdx.x < nkeys) {
@@ -685,24 +808,6 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(const int8_t* 
       running[threadIdx.x] += tot;
     }
     __syncthreads();
-  }
-}
-
-// Active-set sizes of every subiteration level (prefix sums of the per-level
-// counts) for the graph-captured sweep, which reads its counts on device.
-// alias_k1: single-domain run, the K1 list is the K3 list.
-__global__ void k_plan_prefix(PlanDev* plan, int alias_k1) {
-  if (threadIdx.x != 0) return;
-  long long c = 0, f = 0, k = 0;
-  for (int l = 0; l < kMaxLevels; ++l) {
-    if (alias_k1) plan->k1_count[l] = plan->cell_count[l];
-    c += plan->cell_count[l];
-    f += plan->face_count[l];
-    k += plan->k1_count[l];
-    plan->ncell_prefix[l] = (int)c;
-    plan->nface_prefix[l] = (int)f;
-    plan->nk1_prefix[l] = (int)k;
-    plan->gcell_count[l] = plan->cell_count[l];
   }
 }
 

@@ -146,6 +146,7 @@ struct tafv_gpu {
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
   uint8_t* fflag = nullptr;
   double *dtmax = nullptr, *blockmin = nullptr;
+  unsigned* dt_ticket = nullptr;  // last-block ticket of k_dt_max
   int nblk_dt = 0;
   int *cell_counts = nullptr, *face_counts = nullptr;
   int ntile_c = 0, ntile_f = 0;
@@ -243,7 +244,7 @@ struct tafv_gpu {
     void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
-                    fflag, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
+                    fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
                     klist != clist ? klist : nullptr, k1_counts};
     for (void* p : ptrs)
@@ -603,7 +604,10 @@ void alloc_state(tafv_gpu& h) {
   h.raw = dalloc<int8_t>(N);
   h.tmpa = dalloc<int8_t>(N);
   h.tmpb = dalloc<int8_t>(N);
-  h.fflag = dalloc<uint8_t>(N);
+  h.fflag = dalloc<uint8_t>(((size_t)N + 3) & ~(size_t)3);  // word-addressed by k_face_cadence
+  CK(cudaMemset(h.fflag, 0, ((size_t)N + 3) & ~(size_t)3));
+  h.dt_ticket = dalloc<unsigned>(1);
+  CK(cudaMemset(h.dt_ticket, 0, sizeof(unsigned)));
   h.cad = dalloc<int8_t>(F);
   CK(cudaMemset(h.tau, 0, N));
   CK(cudaMemset(h.cad, 0, F));
@@ -746,61 +750,65 @@ void halo_i8(tafv_gpu& h, int8_t* arr) {
 
 // ---- plan ------------------------------------------------------------------
 template <class P>
-void launch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
+void launch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale, bool reset) {
   k_dt_max<P><<<h.nblk_dt, 256, 0, h.st>>>(h.mesh_dev(), h.state_dev(), h.pp, cfl, dt_cap, h.dtmax,
-                                          h.blockmin, tau_scale, h.n_own);
-  k_dt_min<<<1, 256, 0, h.st>>>(h.blockmin, h.nblk_dt, h.dplan);
-  h.launches += 2;
+                                          h.blockmin, tau_scale, h.n_own, h.dt_ticket, h.dplan,
+                                          reset ? 1 : 0);
+  ++h.launches;
   // global stable step: exact min over ranks (RankComm::allreduce_min,
   // exchange.cpp:155-192)
   if (h.sharded()) h.comm->allreduce_min_f64(h.rank, &h.dplan->dt_min, 1, h.st);
 }
 
-void dispatch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale) {
+// reset: also clear the plan's error flag and counts (plan_iteration); dt_min
+// is written, nonfinite/totals (the previous sweep's, read back with this
+// plan) are kept.
+void dispatch_dt_max(tafv_gpu& h, double cfl, double dt_cap, const int8_t* tau_scale, bool reset) {
   switch (h.model) {
-    case TAFV_ADVECTION: launch_dt_max<Advection2D>(h, cfl, dt_cap, tau_scale); break;
-    case TAFV_BURGERS: launch_dt_max<Burgers2D>(h, cfl, dt_cap, tau_scale); break;
-    default: launch_dt_max<Euler3D>(h, cfl, dt_cap, tau_scale); break;
+    case TAFV_ADVECTION: launch_dt_max<Advection2D>(h, cfl, dt_cap, tau_scale, reset); break;
+    case TAFV_BURGERS: launch_dt_max<Burgers2D>(h, cfl, dt_cap, tau_scale, reset); break;
+    default: launch_dt_max<Euler3D>(h, cfl, dt_cap, tau_scale, reset); break;
   }
-}
-
-void reset_plan_counts(tafv_gpu& h) {
-  // Clear the error flags and counts; keep dt_min (written by the dt kernels)
-  // and nonfinite/totals (the previous sweep's, read back with this plan).
-  CK(cudaMemsetAsync(&h.dplan->err, 0, sizeof(int), h.st));
-  CK(cudaMemsetAsync(&h.dplan->cell_count[0], 0, sizeof(long long) * 3 * kMaxLevels, h.st));
 }
 
 // Face cadences, fringe counts and the level-sorted cell / face lists, then
 // the asynchronous read-back of the plan (and of the previous sweep's flags).
-void enqueue_finish_plan(tafv_gpu& h, int nkeys) {
+// cells_counted: the last level sweep already left the cell tile counts and
+// cleared the fringe flags (single-domain plan).
+void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   const MeshDev md = h.mesh_dev();
-  CK(cudaMemsetAsync(h.fflag, 0, h.N, h.st));
-  k_face_cadence<<<h.grid_for(h.F, 256), 256, 0, h.st>>>(md, h.tau, h.cad, h.fflag, h.dplan);
-  // K3 list: owned cells by level (prefixes = active sets of each level)
-  k_tile_count<<<std::max(1, h.ntile_c), kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts,
-                                                                     h.fflag, h.dplan);
-  k_tile_scan<<<1, 1024, 0, h.st>>>(h.cell_counts, std::max(1, h.ntile_c), nkeys, h.dplan->cell_count);
-  k_tile_scatter<<<std::max(1, h.ntile_c), kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts,
-                                                                       h.clist);
-  h.launches += 4;
-  if (h.klist != h.clist) {  // K1 list: owned + ring 1 by level (shards)
-    k_tile_count<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts,
-                                                                       nullptr, h.dplan);
-    k_tile_scan<<<1, 1024, 0, h.st>>>(h.k1_counts, std::max(1, h.ntile_k), nkeys, h.dplan->k1_count);
-    k_tile_scatter<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts,
-                                                                         h.klist);
-    h.launches += 3;
+  const int ntc = std::max(1, h.ntile_c);
+  if (!cells_counted) {
+    CK(cudaMemsetAsync(h.fflag, 0, h.N, h.st));
+    k_tile_count<<<ntc, kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts);
+    ++h.launches;
   }
-  if (h.F_own > 0) {  // K2 list: faces touching an owned cell by cadence
-    k_tile_count<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F_own, nkeys, h.face_counts, nullptr,
-                                                          h.dplan);
-    k_tile_scan<<<1, 1024, 0, h.st>>>(h.face_counts, h.ntile_f, nkeys, h.dplan->face_count);
-    k_tile_scatter<<<h.ntile_f, kCompactThreads, 0, h.st>>>(h.cad, h.F_own, nkeys, h.face_counts, h.flist);
-    h.launches += 3;
+  const bool k1 = h.klist != h.clist;  // shards: K1 list over owned + ring 1
+  if (k1) {
+    k_tile_count<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts);
+    ++h.launches;
   }
-  k_plan_prefix<<<1, 32, 0, h.st>>>(h.dplan, h.klist == h.clist ? 1 : 0);
-  ++h.launches;
+  k_face_cadence<<<std::max(1, (h.F + kTile - 1) / kTile), kCompactThreads, 0, h.st>>>(
+      md, h.tau, h.cad, reinterpret_cast<unsigned*>(h.fflag), h.dplan, h.n_own, h.F_own, nkeys, h.face_counts,
+      h.ntile_f);
+  // K3 list (owned cells by level), K2 list (faces touching owned by cadence),
+  // shards' K1 list: prefixes of each are the active sets of every level
+  CompactJobs jobs{};
+  jobs.j[0] = CompactJob{h.tau, h.n_own, ntc, h.cell_counts, h.clist, &h.dplan->cell_count[0],
+                         &h.dplan->ncell_prefix[0]};
+  jobs.j[1] = CompactJob{h.cad, h.F_own, h.ntile_f, h.face_counts, h.flist, &h.dplan->face_count[0],
+                         &h.dplan->nface_prefix[0]};
+  jobs.njobs = 2;
+  if (k1) {
+    jobs.j[2] = CompactJob{h.tau, h.n_k1, std::max(1, h.ntile_k), h.k1_counts, h.klist,
+                           &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0]};
+    jobs.njobs = 3;
+  }
+  int tiles = 0;
+  for (int q = 0; q < jobs.njobs; ++q) tiles += jobs.j[q].ntiles;
+  k_tile_scan<<<jobs.njobs, 1024, 0, h.st>>>(jobs, nkeys, h.dplan, k1 ? 0 : 1);
+  k_tile_scatter<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
+  h.launches += 3;
   if (h.sharded()) h.comm->allreduce_sum_i64(h.rank, &h.dplan->gcell_count[0], kMaxLevels, h.st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
@@ -902,20 +910,49 @@ void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
 }
 
 void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
-  dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr);
-  reset_plan_counts(h);
+  dispatch_dt_max(h, opt.cfl, opt.dt_cap, nullptr, true);
+  const MeshDev md = h.mesh_dev();
+  const int nkeys = opt.theta_max + 1;
+  if (!h.sharded()) {
+    // classification fused into the first Jacobi sweep, tile counts into the
+    // last (k_level_sweep). The fixpoint is min_d raw(d) + dist(c, d); a cell
+    // more than theta_max hops away cannot lower raw(c) <= theta_max, so
+    // theta_max sweeps reach it exactly (levels.cpp:33-51).
+    const int ntc = std::max(1, h.ntile_c), gs = h.grid_for(h.n_own, 256);
+    const int sweeps = std::max(1, opt.theta_max);
+    const int8_t* src = nullptr;
+    for (int i = 0; i < sweeps; ++i) {
+      const bool first = i == 0, last = i == sweeps - 1;
+      int8_t* dst = last ? h.tau : (i % 2 == 0 ? h.tmpa : h.tmpb);
+      const int sm = opt.theta_max > 0 ? 1 : 0;
+      uint8_t* clr = first ? h.fflag : nullptr;
+      if (first && last)
+        k_level_sweep<true, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+      else if (first)
+        k_level_sweep<true, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+      else if (last)
+        k_level_sweep<false, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+      else
+        k_level_sweep<false, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+      ++h.launches;
+      src = dst;
+    }
+    enqueue_finish_plan(h, nkeys, true);
+    return;
+  }
   k_classify<<<h.grid_for(h.n_own, 256), 256, 0, h.st>>>(h.n_own, h.dtmax, h.dplan, opt.theta_max, h.raw);
   ++h.launches;
   halo_i8(h, h.raw);
-  // Jacobi smoothing (levels.cpp:33-51). The fixpoint is
-  // min_d raw(d) + dist(c, d); a cell more than theta_max hops away cannot
-  // lower raw(c) <= theta_max, so theta_max sweeps reach it exactly.
-  const MeshDev md = h.mesh_dev();
+  // Jacobi smoothing (levels.cpp:33-51), theta_max sweeps as above; shards
+  // sweep the owned cells, then refresh the halo levels (the replicated-array
+  // Jacobi of the reference, levels.hpp:32-37)
   if (opt.theta_max == 0) {
     CK(cudaMemcpyAsync(h.tau, h.raw, h.N, cudaMemcpyDeviceToDevice, h.st));  // raw halo already fresh
   } else {
-    // shards: sweep the owned cells, then refresh the halo levels (the
-    // replicated-array Jacobi of the reference, levels.hpp:32-37)
     const int8_t* src = h.raw;
     for (int i = 0; i < opt.theta_max; ++i) {
       int8_t* dst = i == opt.theta_max - 1 ? h.tau : (i % 2 == 0 ? h.tmpa : h.tmpb);
@@ -925,7 +962,7 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
       src = dst;
     }
   }
-  enqueue_finish_plan(h, opt.theta_max + 1);
+  enqueue_finish_plan(h, nkeys, false);
 }
 
 // After the plan read-back: levels, counts and the stable-step check
@@ -973,9 +1010,9 @@ void inject(tafv_gpu& h, const int32_t* tau_in, double dt, const tafv_options* o
     CK(cudaMemcpyAsync(&h.dplan->dt_min, &h.hplan->dt_min, sizeof(double), cudaMemcpyHostToDevice, h.st));
   } else {
     require(opt != nullptr, "inject_levels: dt <= 0 needs options for the stable step");
-    dispatch_dt_max(h, opt->cfl, opt->dt_cap, h.tau);
+    dispatch_dt_max(h, opt->cfl, opt->dt_cap, h.tau, false);
   }
-  enqueue_finish_plan(h, maxl + 1);
+  enqueue_finish_plan(h, maxl + 1, false);
   CK(cudaEventRecord(h.ev[3], h.st));
   CK(cudaStreamSynchronize(h.st));
   accept_plan(h);
