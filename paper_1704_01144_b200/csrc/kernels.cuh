@@ -452,16 +452,23 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
   }
   if (LAST) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) plan->nonfinite = 1;
-    __shared__ DD red[128];
-    red[threadIdx.x] = acc;
+    // fixed-shape reduction: lane k of each warp merges its component's lanes
+    // k + NV*j (j = 1 .. CPW-1) in order, then thread k merges the warps
+    DD a = acc;
+#pragma unroll
+    for (int jj = 1; jj < CPW; ++jj) {
+      DD o;
+      o.hi = __shfl_sync(0xffffffffu, acc.hi, (lane + jj * NV) & 31);
+      o.lo = __shfl_sync(0xffffffffu, acc.lo, (lane + jj * NV) & 31);
+      if (lane < NV) a = dd_merge(a, o);
+    }
+    __shared__ DD wred[4][NV];
+    if (lane < NV) wred[threadIdx.x >> 5][lane] = a;
     __syncthreads();
-    if (threadIdx.x < NV) {  // component k = threadIdx.x: its lanes, in thread order
-      DD a{0.0, 0.0};
-      for (int t = threadIdx.x; t < blockDim.x; ++t) {
-        const int l = t & 31, jj = l / NV;
-        if (jj < CPW && l - jj * NV == (int)threadIdx.x) a = dd_merge(a, red[t]);
-      }
-      partials[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = a;
+    if (threadIdx.x < NV) {
+      DD b = wred[0][threadIdx.x];
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q) b = dd_merge(b, wred[q][threadIdx.x]);
+      partials[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = b;
     }
   }
 }
