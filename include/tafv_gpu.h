@@ -125,7 +125,10 @@ void tafv_gpu_destroy(tafv_gpu* h);
 const char* tafv_gpu_last_error(const tafv_gpu* h);
 
 /* State in/out (SolverState::w, ::W, ::t0, ::iteration). W == NULL means
- * W = w * V, i.e. init_* + sync_extensive (state.cpp:46-68). */
+ * W = w * V, i.e. init_* + sync_extensive (state.cpp:46-68); w == NULL means
+ * w = W / V, the relation every corrector leaves (intensive_correct,
+ * kernels.cpp:237-241), so a state saved as W alone after an iteration is
+ * restored bitwise. get_state skips a NULL output. */
 int tafv_gpu_set_state(tafv_gpu* h, const double* w, const double* W, double t0,
                        int32_t iteration);
 int tafv_gpu_get_state(tafv_gpu* h, double* w, double* W, double* t0, int32_t* iteration);

@@ -178,11 +178,16 @@ class Solver:
 
     # -- state ---------------------------------------------------------------
     def set_state(self, w, W=None, t0=0.0, iteration=0):
-        """SolverState w/W/t0/iteration; W=None -> W = w*V (sync_extensive)."""
-        w = _f64(w).reshape(-1)
-        assert w.size == self.nc * self.nv
+        """SolverState w/W/t0/iteration; W=None -> W = w*V (sync_extensive);
+        w=None -> w = W/V (the relation every corrector leaves)."""
+        if w is None and W is None:
+            raise InvalidArgument("set_state: w and W are both None")
+        wa = None if w is None else _f64(w).reshape(-1)
         Wa = None if W is None else _f64(W).reshape(-1)
-        self._c(self.lib.tafv_gpu_set_state(self.h, _ptr(w), _ptr(Wa), float(t0), int(iteration)))
+        for a in (wa, Wa):
+            if a is not None and a.size != self.nc * self.nv:
+                raise InvalidArgument("set_state: wrong state size")
+        self._c(self.lib.tafv_gpu_set_state(self.h, _ptr(wa), _ptr(Wa), float(t0), int(iteration)))
 
     def get_state(self):
         """(w, W, t0, iteration); a shard fills only its owned rows (zeros elsewhere)."""

@@ -871,6 +871,14 @@ __global__ void k_scatter_rows(const double* src, const int* perm, int n, int wi
 }
 
 // W = w * V (sync_extensive, state.cpp:61-68) for set_state without W.
+// w = W / V (intensive_correct, kernels.cpp:237-241)
+__global__ void k_intensive(const double* W, const double* vol, int n, int nv, double* w) {
+  const size_t total = (size_t)n * nv;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+    w[i] = W[i] / vol[i / nv];
+}
+
 __global__ void k_sync_extensive(const double* w, const double* vol, int n, int nv, double* W) {
   const size_t total = (size_t)n * nv;
   const size_t stride = (size_t)gridDim.x * blockDim.x;

@@ -1422,30 +1422,32 @@ const char* tafv_gpu_last_error(const tafv_gpu* h) {
 int tafv_gpu_set_state(tafv_gpu* h, const double* w_in, const double* W_in, double t0,
                        int32_t iteration) {
   return guard(h, [&] {
-    require(w_in != nullptr, "set_state: w is null");
+    require(w_in != nullptr || W_in != nullptr, "set_state: w and W are both null");
     // shards take the GLOBAL state and keep their local cells' rows
     std::vector<double> wl, Wl;
     const double* w = w_in;
     const double* W = W_in;
     if (h->sharded()) {
-      wl.resize((size_t)h->N * h->nv);
-      for (int i = 0; i < h->N; ++i)
-        std::memcpy(&wl[(size_t)i * h->nv], w_in + (size_t)h->shard_cells[i] * h->nv, h->nv * sizeof(double));
-      w = wl.data();
-      if (W_in) {
-        Wl.resize(wl.size());
+      auto local = [&](const double* src, std::vector<double>& dst) {
+        dst.resize((size_t)h->N * h->nv);
         for (int i = 0; i < h->N; ++i)
-          std::memcpy(&Wl[(size_t)i * h->nv], W_in + (size_t)h->shard_cells[i] * h->nv, h->nv * sizeof(double));
-        W = Wl.data();
-      }
+          std::memcpy(&dst[(size_t)i * h->nv], src + (size_t)h->shard_cells[i] * h->nv, h->nv * sizeof(double));
+        return dst.data();
+      };
+      if (w_in) w = local(w_in, wl);
+      if (W_in) W = local(W_in, Wl);
     }
     const size_t n = (size_t)h->N * h->nv;
     double* stage = h->staging(n);
-    CK(cudaMemcpyAsync(stage, w, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
-    k_gather_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(stage, h->d_cperm, h->N, h->nv, h->w);
+    if (w) {
+      CK(cudaMemcpyAsync(stage, w, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
+      k_gather_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(stage, h->d_cperm, h->N, h->nv, h->w);
+    }
     if (W) {
       CK(cudaMemcpyAsync(stage, W, n * sizeof(double), cudaMemcpyHostToDevice, h->st));
       k_gather_rows<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(stage, h->d_cperm, h->N, h->nv, h->W);
+      if (!w)  // w = W / V, the relation every corrector leaves (kernels.cpp:237-241)
+        k_intensive<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->W, h->vol, h->N, h->nv, h->w);
     } else {
       k_sync_extensive<<<h->grid_for((long long)n, 256), 256, 0, h->st>>>(h->w, h->vol, h->N, h->nv, h->W);
     }

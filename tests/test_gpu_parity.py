@@ -254,6 +254,26 @@ def test_window_alias_is_invisible(cid, scale, gpu):
         assert a.tobytes() == b.tobytes()
 
 
+def test_state_round_trip_as_extensive_only(gpu):
+    """set_state(None, W) rebuilds w = W / V: after whole iterations that is
+    bitwise the solver's own w, and the continued run is identical."""
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    a = Solver(mesh, "euler")
+    a.set_state(cfg.initial_state(mesh))
+    a.reference_integrate(cfg.options(), 2)
+    w, W, t0, it = a.get_state()
+    b = Solver(mesh, "euler")
+    b.set_state(None, W, t0, it)
+    wb, Wb, t0b, itb = b.get_state()
+    assert wb.tobytes() == w.tobytes() and Wb.tobytes() == W.tobytes() and (t0b, itb) == (t0, it)
+    ra, rb = a.reference_integrate(cfg.options(), 2), b.reference_integrate(cfg.options(), 2)
+    assert [r["dt"] for r in ra] == [r["dt"] for r in rb]
+    assert a.get_state()[0].tobytes() == b.get_state()[0].tobytes()
+    with pytest.raises(InvalidArgument):
+        b.set_state(None, None)
+
+
 def test_cpp_shim_caller(gpu):
     """A reference-style C++ caller (include/tafv_gpu.hpp) integrates on the
     GPU and sees the reference's exception classes."""
