@@ -644,6 +644,11 @@ void set_grids_t(tafv_gpu& h) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_face_flux<P, true>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_gather_update<P, true, false, DEG>, 128, 0));
   h.grid_k1 = h.sms * std::max(1, b1);
+  // trailing corrector: exactly one wave of resident blocks (its partials
+  // buffer holds sms * 16 blocks)
+  int bl = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, k_gather_update<P, false, true, DEG>, 128, 0));
+  h.nblk_last = h.sms * std::max(1, std::min(16, bl));
   h.grid_k2 = h.sms * std::max(1, b2);
   h.grid_k3 = h.sms * std::max(1, b3);
 }
