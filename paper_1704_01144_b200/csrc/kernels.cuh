@@ -57,7 +57,7 @@ struct MeshDev {
   // and the limiter's face-centroid offset fc - cc (same IEEE values the
   // kernel would compute: sign*area is exact, the subtraction is the same).
   const double4* __restrict__ sgeo;  // [N*6]
-  const double* __restrict__ sdx;    // [N*6][3]
+  const double4* __restrict__ sdx;   // [N*6] {dx, dy, dz, 0}: one 256-bit load per slot
 };
 
 struct StateDev {
@@ -125,6 +125,23 @@ __device__ __forceinline__ int stage_spec(const StateDev& s, int x, int front, b
   return tx;
 }
 
+// One 256-bit load of a 32-byte aligned double4 (sm_100), read-only path.
+#ifndef TAFV_V4
+#define TAFV_V4 2
+#endif
+__device__ __forceinline__ double4 ld4(const double4* p) {
+  double4 r;
+#if TAFV_V4 == 2
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+#elif TAFV_V4 == 1
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+#else
+  r = *p;
+#endif
+  return r;
+}
+
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
 __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
 
@@ -190,11 +207,11 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       double4 gm;
       double scale;
       if (DEG == 6 && m.sgeo) {
-        gm = m.sgeo[t];
+        gm = ld4(m.sgeo + t);
         scale = gm.w;
       } else {
         const int ef = m.adj_face[t];
-        gm = m.geo[slot_face(ef)];
+        gm = ld4(m.geo + slot_face(ef));
         scale = slot_sign(ef) * gm.w;
       }
       double wf[NV];
@@ -246,10 +263,10 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       for (int t = s0; t < s1; ++t) {
         double dx0, dx1, dx2;
         if (DEG == 6 && m.sdx) {
-          const double* d = m.sdx + 3 * (size_t)t;
-          dx0 = d[0];
-          dx1 = d[1];
-          dx2 = d[2];
+          const double4 d = ld4(m.sdx + t);
+          dx0 = d.x;
+          dx1 = d.y;
+          dx2 = d.z;
         } else {
           const int f = slot_face(m.adj_face[t]);
           const double* fc = m.fcen + 3 * (size_t)f;
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     const int i = rev ? n - 1 - ii : ii;
     const int f = list ? list[i] : i;
     const int2 lr = m.lr[f];
-    const double4 gm = m.geo[f];
+    const double4 gm = ld4(m.geo + f);
     const double nrm[3] = {gm.x, gm.y, gm.z};
     const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
     double wL[NV], wR[NV];

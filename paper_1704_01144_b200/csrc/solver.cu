@@ -135,7 +135,7 @@ struct tafv_gpu {
   int* rcf = nullptr;
   double4* geo = nullptr;
   double4* sgeo = nullptr;  // hex fast path per-slot geometry (see MeshDev)
-  double* sdx = nullptr;
+  double4* sdx = nullptr;
   bool slot_geo = true;
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
@@ -543,17 +543,18 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
   for (int i = 0; i <= h.n_k1 && h.deg6; ++i) h.deg6 = off[i] == 6 * i;
   if (h.deg6) {
     std::vector<double4> sgeo(h.M);
-    std::vector<double> sdx(3 * (size_t)h.M);
+    std::vector<double4> sdx(h.M, make_double4(0.0, 0.0, 0.0, 0.0));
     for (int i = 0; i < h.n_k1; ++i)
       for (int t = 6 * i; t < 6 * i + 6; ++t) {
         const int j = adj_face[t] >= 0 ? adj_face[t] : ~adj_face[t];
         const double4 g = geo[j];
         sgeo[t] = make_double4(g.x, g.y, g.z, sgn[t] * g.w);
-        for (int d = 0; d < 3; ++d) sdx[3 * (size_t)t + d] = fcen[3 * (size_t)j + d] - cen[3 * (size_t)i + d];
+        sdx[t] = make_double4(fcen[3 * (size_t)j] - cen[3 * (size_t)i], fcen[3 * (size_t)j + 1] - cen[3 * (size_t)i + 1],
+                              fcen[3 * (size_t)j + 2] - cen[3 * (size_t)i + 2], 0.0);
       }
     h.sgeo = dalloc<double4>(h.M);
     up(h.sgeo, sgeo);
-    h.sdx = dalloc<double>(3 * (size_t)h.M);
+    h.sdx = dalloc<double4>(h.M);
     up(h.sdx, sdx);
   }
   h.cen = dalloc<double>(3 * (size_t)N);
