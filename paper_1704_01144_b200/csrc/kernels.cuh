@@ -142,6 +142,23 @@ __device__ __forceinline__ double4 ld4(const double4* p) {
   return r;
 }
 
+// 256-bit load through L1 (rows reused by neighbouring items) and store.
+__device__ __forceinline__ double4 ld4a(const double* p) {
+  double4 r;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+// Gradient rows are padded to a multiple of 4 doubles (Euler: 15 -> 16) so
+// K1 writes and K2 reads them with 256-bit accesses.
+template <int NV>
+struct GradRow {
+  static constexpr int S = (NV * 3 + 3) / 4 * 4;
+};
+
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
 __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
 
@@ -286,13 +303,19 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #pragma unroll
         for (int d = 0; d < D; ++d) g[k][d] *= alpha[k];
     }
-    double* go = s.grad + (size_t)c * NV * 3;
+    constexpr int GS = GradRow<NV>::S;
+    double row[GS];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      go[3 * k] = g[k][0];
-      go[3 * k + 1] = g[k][1];
-      go[3 * k + 2] = D == 3 ? g[k][D - 1] : 0.0;
+      row[3 * k] = g[k][0];
+      row[3 * k + 1] = g[k][1];
+      row[3 * k + 2] = D == 3 ? g[k][D - 1] : 0.0;
     }
+#pragma unroll
+    for (int q = 3 * NV; q < GS; ++q) row[q] = 0.0;
+    double* go = s.grad + (size_t)c * GS;
+#pragma unroll
+    for (int q = 0; q < GS; q += 4) st4(go + q, row[q], row[q + 1], row[q + 2], row[q + 3]);
   }
 }
 
@@ -300,10 +323,24 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 template <int D>
 __device__ __forceinline__ double extrapolate(double w, const double* g, const double* from,
                                               const double* to) {
-  // g: a gradient row, read-only in K2 (only K1 writes it)
-  double v = (w + __ldg(g) * (to[0] - from[0])) + __ldg(g + 1) * (to[1] - from[1]);
-  if (D == 3) v = v + __ldg(g + D - 1) * (to[D - 1] - from[D - 1]);
+  double v = (w + g[0] * (to[0] - from[0])) + g[1] * (to[1] - from[1]);
+  if (D == 3) v = v + g[D - 1] * (to[D - 1] - from[D - 1]);
   return v;
+}
+
+// A cell's gradient row into registers (read-only in K2: only K1 writes it).
+template <int NV>
+__device__ __forceinline__ void load_grad(const StateDev& s, int x, double* g) {
+  constexpr int GS = GradRow<NV>::S;
+  const double* src = s.grad + (size_t)x * GS;
+#pragma unroll
+  for (int q = 0; q < GS; q += 4) {
+    const double4 v = ld4a(src + q);
+    g[q] = v.x;
+    g[q + 1] = v.y;
+    g[q + 2] = v.z;
+    g[q + 3] = v.w;
+  }
 }
 
 // ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
@@ -331,7 +368,8 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     {
       double we[NV];
       tl = stage_spec<NV>(s, lr.x, front, PRED, we);
-      const double* g = s.grad + (size_t)lr.x * NV * 3;
+      double g[GradRow<NV>::S];
+      load_grad<NV>(s, lr.x, g);
       const double cl[3] = {m.cen[3 * (size_t)lr.x], m.cen[3 * (size_t)lr.x + 1], m.cen[3 * (size_t)lr.x + 2]};
 #pragma unroll
       for (int k = 0; k < NV; ++k) wL[k] = extrapolate<D>(we[k], g + 3 * k, cl, fc);
@@ -347,7 +385,8 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
       const int tr = stage_spec<NV>(s, lr.y, front, PRED, we);
       eq = tr == tl;
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
-      const double* g = s.grad + (size_t)lr.y * NV * 3;
+      double g[GradRow<NV>::S];
+      load_grad<NV>(s, lr.y, g);
       const double cr[3] = {m.cen[3 * (size_t)lr.y], m.cen[3 * (size_t)lr.y + 1], m.cen[3 * (size_t)lr.y + 2]};
       const double* to = m.fcen + 3 * (size_t)(m.rcf ? m.rcf[f] : f);
       const double tc[3] = {to[0], to[1], to[2]};

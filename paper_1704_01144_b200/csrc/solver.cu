@@ -140,6 +140,7 @@ struct tafv_gpu {
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
+  size_t gs = 0;  // gradient row stride in doubles (padded, see GradRow)
   double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
   uint8_t* ialias = nullptr;  // [F] see StateDev::ialias
   bool iwin_alias = true;
@@ -588,14 +589,15 @@ void alloc_state(tafv_gpu& h) {
   h.w = dalloc<double>(N * nv);
   h.W = dalloc<double>(N * nv);
   h.wp = dalloc<double>(N * nv);
-  h.grad = dalloc<double>(N * nv * 3);
+  h.gs = (nv * 3 + 3) / 4 * 4;  // GradRow<NV>::S
+  h.grad = dalloc<double>(N * h.gs);
   h.phi = dalloc<double>(F * nv);
   h.isub = dalloc<double>(F * nv);
   h.iwin = dalloc<double>(F * nv);
   CK(cudaMemset(h.w, 0, N * nv * sizeof(double)));
   CK(cudaMemset(h.W, 0, N * nv * sizeof(double)));
   CK(cudaMemset(h.wp, 0, N * nv * sizeof(double)));
-  CK(cudaMemset(h.grad, 0, N * nv * 3 * sizeof(double)));
+  CK(cudaMemset(h.grad, 0, N * h.gs * sizeof(double)));
   CK(cudaMemset(h.phi, 0, F * nv * sizeof(double)));
   CK(cudaMemset(h.isub, 0, F * nv * sizeof(double)));
   CK(cudaMemset(h.iwin, 0, F * nv * sizeof(double)));
@@ -1613,7 +1615,14 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     if (n == "w") rows(h->w, h->N, h->nv, h->d_cperm);
     else if (n == "W") rows(h->W, h->N, h->nv, h->d_cperm);
     else if (n == "w_pred") rows(h->wp, h->N, h->nv, h->d_cperm);
-    else if (n == "grad") rows(h->grad, h->N, h->nv * 3, h->d_cperm);
+    else if (n == "grad") {  // unpadded rows of nv*3
+      const size_t w3 = (size_t)h->nv * 3;
+      double* dense = dalloc<double>((size_t)h->N * w3);
+      CK(cudaMemcpy2DAsync(dense, w3 * sizeof(double), h->grad, h->gs * sizeof(double), w3 * sizeof(double),
+                           h->N, cudaMemcpyDeviceToDevice, h->st));
+      rows(dense, h->N, (int)w3, h->d_cperm);
+      cudaFree(dense);
+    }
     else if (n == "dt_max") rows(h->dtmax, h->N, 1, h->d_cperm);
     else if (n == "phi_pred") rows(h->phi, h->F, h->nv, h->d_fperm);
     else if (n == "int_substep") rows(h->isub, h->F, h->nv, h->d_fperm);
