@@ -57,6 +57,7 @@ class Config:
     dt_cap: float = 1e30
     synthetic_levels: float | None = None  # tau=0 fraction for config 5
     tiles: int = 1  # weak-scaling copies of the unit-cube config along x
+    periodic: tuple = ()  # axes with periodic boundaries (meshgen.make_periodic)
     extra: dict = field(default_factory=dict)
 
     @property
@@ -87,7 +88,8 @@ class Config:
 
     def mesh(self):
         x, y, z = self.nodes()
-        return meshgen.hex_mesh(x, y, z, jitter=self.jitter, seed=self.seed, permute=self.permute)
+        m = meshgen.hex_mesh(x, y, z, jitter=self.jitter, seed=self.seed, permute=self.permute)
+        return meshgen.make_periodic(m, self.periodic) if self.periodic else m
 
     def initial_state(self, mesh):
         c = mesh["cen"]
@@ -186,3 +188,12 @@ CONFIGS = {
 def get(i, scale=1):
     c = CONFIGS[int(i)]
     return c if scale == 1 else c.scaled(scale)
+
+
+def periodic_blast():
+    """Test workload (not a BASELINE config): a 10x8x6 hex mesh graded in z,
+    periodic in x and y, with a blast straddling the x-periodic boundary --
+    exercises partner faces in the Euler path."""
+    return Config("periodic-blast", (10, 8, 6), "wall_z", (1.15,), 0.0, True, "blast",
+                  dict(centre=(0.95, 0.5, 0.3), radius=0.2, rho_in=2.0, p_in=10.0), 2, 0.25, 4, 77,
+                  periodic=(0, 1))

@@ -48,19 +48,26 @@ void partition_slabs(const tafv_mesh_view& m, int nranks, int axis, const double
 
 Shard build_shard(const tafv_mesh_view& m, const int32_t* rank_of_cell, int rank, int nranks) {
   const int N = m.n_cells, F = m.n_faces;
-  for (int f = 0; f < F; ++f)
-    if (m.face_partner[f] >= 0)
-      throw std::invalid_argument("shard: periodic meshes are not supported by the multi-GPU path");
+  // resolved right cell (kernels.cpp:15-20): the right cell, or across a
+  // periodic boundary the partner face's left cell, or -1 (transmissive)
+  auto rright = [&](int f) {
+    if (m.face_right[f] >= 0) return m.face_right[f];
+    return m.face_partner[f] >= 0 ? m.face_left[m.face_partner[f]] : -1;
+  };
   for (int c = 0; c < N; ++c)
     if (rank_of_cell[c] < 0 || rank_of_cell[c] >= nranks)
       throw std::invalid_argument("shard: rank_of_cell out of range");
   // neighbour CSR (global)
+  // (a periodic link appears once from each of its two boundary faces)
   std::vector<int> off(N + 1, 0);
-  for (int f = 0; f < F; ++f)
+  for (int f = 0; f < F; ++f) {
     if (m.face_right[f] >= 0) {
       ++off[m.face_left[f] + 1];
       ++off[m.face_right[f] + 1];
+    } else if (m.face_partner[f] >= 0) {
+      ++off[m.face_left[f] + 1];
     }
+  }
   for (int c = 0; c < N; ++c) off[c + 1] += off[c];
   std::vector<int> nb(off[N]);
   {
@@ -69,6 +76,8 @@ Shard build_shard(const tafv_mesh_view& m, const int32_t* rank_of_cell, int rank
       if (m.face_right[f] >= 0) {
         nb[cur[m.face_left[f]]++] = m.face_right[f];
         nb[cur[m.face_right[f]]++] = m.face_left[f];
+      } else if (m.face_partner[f] >= 0) {
+        nb[cur[m.face_left[f]]++] = rright(f);
       }
   }
   // ring classes per rank q: 0 owned, 1 ring 1, 2 ring 2, 3 absent
@@ -97,10 +106,14 @@ Shard build_shard(const tafv_mesh_view& m, const int32_t* rank_of_cell, int rank
       else if (mine[c] == 1) ++s.n_r1;
       else ++s.n_r2;
     }
+  // faces with a side in owned or ring 1 (a kept periodic face's partner is
+  // kept too: its sides are the same two cells)
+  std::vector<int> lface(F, -1);
   for (int f = 0; f < F; ++f) {
-    const int l = m.face_left[f], r = m.face_right[f];
+    const int l = m.face_left[f], r = rright(f);
     const bool keep = mine[l] <= 1 || (r >= 0 && mine[r] <= 1);
     if (!keep) continue;
+    lface[f] = (int)s.faces.size();
     s.faces.push_back(f);
     s.touch_own.push_back(mine[l] == 0 || (r >= 0 && mine[r] == 0) ? 1 : 0);
   }
@@ -126,6 +139,11 @@ Shard build_shard(const tafv_mesh_view& m, const int32_t* rank_of_cell, int rank
     s.fr[j] = m.face_right[f] >= 0 ? local[m.face_right[f]] : -1;
     if (s.fl[j] < 0 || (m.face_right[f] >= 0 && s.fr[j] < 0))
       throw std::logic_error("shard: face side outside the local cell set");
+    if (m.face_right[f] < 0 && m.face_partner[f] >= 0) {
+      s.fp[j] = lface[m.face_partner[f]];
+      if (s.fp[j] < 0 || local[rright(f)] < 0)
+        throw std::logic_error("shard: periodic partner outside the local face set");
+    }
     s.fa[j] = m.face_area[f];
     for (int d = 0; d < 3; ++d) {
       s.fn[3 * (size_t)j + d] = m.face_normal[3 * (size_t)f + d];

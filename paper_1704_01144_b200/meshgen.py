@@ -46,6 +46,33 @@ def hex_mesh(x, y, z, jitter=0.0, seed=0, permute=False):
     return m
 
 
+def make_periodic(mesh, axes, tol=1e-12):
+    """Link the boundary faces of opposite domain sides along `axes` as
+    periodic partners (Face::periodic_partner, mesh.hpp:26-65; the reference
+    2D generator's torus, mesh.cpp:302-317): face f on the low side and face
+    g on the high side with the same centroid in the other coordinates get
+    fp[f] = g, fp[g] = f; both keep their single cell (right = -1). Needs
+    matching boundary nodes on the two sides (no boundary jitter)."""
+    m = dict(mesh)
+    fp = mesh["fp"].copy()
+    fc, fr = mesh["fc"], mesh["fr"]
+    bnd = np.flatnonzero(fr < 0)
+    for a in axes:
+        lo, hi = fc[bnd, a].min(), fc[bnd, a].max()
+        low = bnd[np.abs(fc[bnd, a] - lo) < tol]
+        high = bnd[np.abs(fc[bnd, a] - hi) < tol]
+        others = [d for d in range(3) if d != a]
+        key = lambda f: tuple(np.round(fc[f, others], 9))
+        index = {key(g): g for g in high}
+        if len(index) != len(high) or len(low) != len(high):
+            raise ValueError("make_periodic: sides do not match")
+        for f in low:
+            g = index[key(f)]
+            fp[f], fp[g] = g, f
+    m["fp"] = fp
+    return m
+
+
 def uniform_nodes(n):
     return np.linspace(0.0, 1.0, n + 1)
 

@@ -60,8 +60,11 @@ def describe(mesh, rank_of_cell, rank, nranks):
     owned = roc[cells] == rank
     g2l = np.full(len(roc), -1, dtype=np.int64)
     g2l[cells] = np.arange(len(cells))
-    fl, fr = g2l[mesh["fl"][faces]], mesh["fr"][faces]
-    fr = np.where(fr >= 0, g2l[np.maximum(fr, 0)], -1)
+    # resolved right (kernels.cpp:15-20): right cell, or the periodic partner's left
+    gfr, gfp = mesh["fr"][faces], mesh["fp"][faces]
+    rr = np.where(gfr >= 0, gfr, np.where(gfp >= 0, mesh["fl"][np.maximum(gfp, 0)], -1))
+    fl = g2l[mesh["fl"][faces]]
+    fr = np.where(rr >= 0, g2l[np.maximum(rr, 0)], -1)
     cls = np.where(owned, 0, 2).astype(np.int8)
     inner = fr >= 0
     a, b = fl[inner], fr[inner]
@@ -77,12 +80,15 @@ def local_mesh(mesh, sh):
     cells, faces = sh["cells"], sh["faces"]
     g2l = np.full(len(mesh["vol"]), -1, dtype=np.int32)
     g2l[cells] = np.arange(len(cells), dtype=np.int32)
+    f2l = np.full(len(mesh["fl"]), -1, dtype=np.int32)
+    f2l[faces] = np.arange(len(faces), dtype=np.int32)
     fr = mesh["fr"][faces]
+    fp = mesh["fp"][faces]
     return {
         "dim": mesh["dim"], "vol": mesh["vol"][cells], "cen": mesh["cen"][cells], "chl": mesh["chl"][cells],
         "fl": g2l[mesh["fl"][faces]], "fr": np.where(fr >= 0, g2l[np.maximum(fr, 0)], -1).astype(np.int32),
-        "fp": np.full(len(faces), -1, dtype=np.int32), "fn": mesh["fn"][faces], "fa": mesh["fa"][faces],
-        "fc": mesh["fc"][faces],
+        "fp": np.where(fp >= 0, f2l[np.maximum(fp, 0)], -1).astype(np.int32), "fn": mesh["fn"][faces],
+        "fa": mesh["fa"][faces], "fc": mesh["fc"][faces],
     }
 
 

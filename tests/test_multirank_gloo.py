@@ -61,7 +61,7 @@ def _rank_main(rank, world, port, cid, scale, iters, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import OracleMesh, OracleSolver
     from paper_1704_01144_b200 import configs, shard
-    cfg = configs.get(cid, scale)
+    cfg = configs.periodic_blast() if cid == "P" else configs.get(cid, scale)
     mesh = cfg.mesh()
     w0 = cfg.initial_state(mesh)
     roc = shard.partition_slabs(mesh, world, axis=0)
@@ -160,11 +160,11 @@ def _run(world, cid, scale, iters):
     return dict(out)
 
 
-@pytest.mark.parametrize("world,cid,scale,iters", [(2, 2, 5, 3), (3, 3, 10, 2), (2, 4, 20, 2)])
+@pytest.mark.parametrize("world,cid,scale,iters", [(2, 2, 5, 3), (3, 3, 10, 2), (2, 4, 20, 2), (2, "P", 1, 3)])
 def test_decomposed_run_matches_single_domain_bitwise(world, cid, scale, iters):
     from oracle import OracleSolver
     from paper_1704_01144_b200 import configs
-    cfg = configs.get(cid, scale)
+    cfg = configs.periodic_blast() if cid == "P" else configs.get(cid, scale)
     mesh = cfg.mesh()
     w0 = cfg.initial_state(mesh)
     ref = OracleSolver(mesh, "euler")
