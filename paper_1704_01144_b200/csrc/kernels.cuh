@@ -606,8 +606,9 @@ __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParam
 }
 
 // levels.cpp:18-25: raw = ratio >= 1 ? ilogb(ratio) : 0, clamped.
-__device__ __forceinline__ int classify_raw(double dt_max, double dt_min, int theta_max) {
-  const double ratio = dt_max / dt_min;
+// y = rcp_div(dt_min): the quotient is bitwise dt_max / dt_min (div_by).
+__device__ __forceinline__ int classify_raw(double dt_max, double dt_min, double y, int theta_max) {
+  const double ratio = div_by(dt_max, dt_min, y);
   int raw = 0;
   if (ratio >= 1.0) {
     const long long bits = __double_as_longlong(ratio);
@@ -621,9 +622,10 @@ __global__ void k_classify(int n, const double* dt_max, const PlanDev* plan, int
                            int8_t* raw) {
   const double dt_min = plan->dt_min;
   const bool ok = dt_min > 0.0 && isfinite(dt_min);
+  const double y = rcp_div(dt_min);
   const int stride = gridDim.x * blockDim.x;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride)
-    raw[c] = ok ? (int8_t)classify_raw(dt_max[c], dt_min, theta_max) : (int8_t)0;
+    raw[c] = ok ? (int8_t)classify_raw(dt_max[c], dt_min, y, theta_max) : (int8_t)0;
 }
 
 // levels.cpp:33-46 one Jacobi sweep: out = min(in, 1 + min over neighbours).
@@ -663,14 +665,15 @@ __global__ void __launch_bounds__(kCompactThreads) k_level_sweep(MeshDev m, cons
                                                                  int theta_max, int smooth, int8_t* out,
                                                                  int n, int nkeys, int* counts,
                                                                  uint8_t* clear_flag) {
-  double dt_min = 0.0;
+  double dt_min = 0.0, y = 0.0;
   bool ok = false;
   if (FIRST) {
     dt_min = plan->dt_min;
     ok = dt_min > 0.0 && isfinite(dt_min);
+    y = rcp_div(dt_min);
   }
   auto lev = [&](int x) -> int {
-    if (FIRST) return ok ? classify_raw(dt_max[x], dt_min, theta_max) : 0;
+    if (FIRST) return ok ? classify_raw(dt_max[x], dt_min, y, theta_max) : 0;
     return in[x];
   };
   __shared__ int cnt[kMaxLevels];
