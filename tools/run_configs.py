@@ -23,7 +23,19 @@ def c_eff(r):
     return sum(n << (r["theta"] - l) for l, n in enumerate(r["level_cells"]))
 
 
+def load_peak():
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
 def run(cfg, iters, tau0=None):
+    """One warm-up iteration (graph capture; excluded), then `iters` timed
+    iterations as plan_iteration + run_iteration (device time of both from
+    the library's events) with the plan's C_eff / F_eff / R_eff for the
+    BASELINE.md byte model B_iter = 1220 C_eff + 568 F_eff + 312 R_eff."""
     t = time.perf_counter()
     mesh = cfg.mesh()
     t_mesh = time.perf_counter() - t
@@ -33,30 +45,39 @@ def run(cfg, iters, tau0=None):
     t_up = time.perf_counter() - t
     s.set_state(w0)
     opt = cfg.options()
-    recs = []
-    t = time.perf_counter()
-    ms = 0.0
+    tau = None
     if cfg.synthetic_levels is not None:
         import copy
         c2 = copy.deepcopy(cfg)
         c2.synthetic_levels = tau0 if tau0 is not None else cfg.synthetic_levels
         tau = c2.levels(mesh)
-        for _ in range(iters):
-            s.inject_levels(tau, -1.0, opt)
-            recs.append(s.run_iteration())
-            ms += s.stats()["ms_sweep"]
-    else:
-        recs = s.reference_integrate(opt, iters)
-        ms = s.stats()["ms_total"]
+
+    def plan():
+        return s.inject_levels(tau, -1.0, opt) if tau is not None else s.plan_iteration(opt)
+
+    plan()
+    s.run_iteration()  # warm-up: graph instantiation
+    recs, ce, fe, re_ = [], 0, 0, 0
+    ms = 0.0
+    t = time.perf_counter()
+    for _ in range(iters):
+        info = plan()
+        ms += s.stats()["ms_plan"]        # this plan's device time
+        ce, fe, re_ = ce + info["c_eff"], fe + info["f_eff"], re_ + info["r_eff"]
+        recs.append(s.run_iteration())
+        ms += s.stats()["ms_sweep"]       # run_iteration resets the stats first
     wall = time.perf_counter() - t
     w, W, t0, it = s.get_state()
     rho = w[:, 0]
     p = 0.4 * (w[:, 4] - 0.5 * (w[:, 1] ** 2 + w[:, 2] ** 2 + w[:, 3] ** 2) / rho)
-    ce = sum(c_eff(r) for r in recs)
+    b_iter = 1220 * ce + 568 * fe + 312 * re_
     out = {
         "config": cfg.name, "cells": len(mesh["vol"]), "faces": len(mesh["fa"]), "iterations": iters,
         "tau0_share": tau0, "t_end": t0, "cell_updates": ce,
         "device_ms": round(ms, 3), "cell_updates_per_s": ce / (ms / 1e3) if ms else None,
+        "byte_model_GBps": round(b_iter / (ms / 1e3) / 1e9, 1) if ms else None,
+        "byte_model_frac": round(b_iter / (ms / 1e3) / 1e9 / load_peak(), 3) if ms else None,
+        "f_eff_over_c_eff": round(fe / ce, 3),
         "wall_s": round(wall, 3), "mesh_gen_s": round(t_mesh, 2), "upload_s": round(t_up, 2),
         "levels_first": recs[0]["level_cells"], "levels_last": recs[-1]["level_cells"],
         "theta": [r["theta"] for r in recs][:3] + ["..."],
