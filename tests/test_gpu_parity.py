@@ -15,7 +15,7 @@ import pytest
 
 from conftest import golden_names, golden_plan_lists, load_golden
 from paper_1704_01144_b200 import Diverged, InvalidArgument, LogicError, Solver, SolverOptions
-from paper_1704_01144_b200 import configs
+from paper_1704_01144_b200 import configs, meshgen
 
 pytestmark = pytest.mark.gpu
 
@@ -372,6 +372,61 @@ def test_sharded_loopback_matches_single_domain_bitwise(cid, scale, world, iters
         for a, b in zip(recs, ref):
             for x, y in zip(a["total_extensive"], b["total_extensive"]):
                 assert abs(x - y) <= 1e-12 * max(1.0, abs(y))
+
+
+@pytest.mark.slow
+def test_sharded_full_size_config2_bitwise(gpu):
+    """Config 2 at its full size (1M cells) as 4 slab shards: bitwise the
+    single-domain run (a size-independent decomposition invariant)."""
+    cfg = configs.get(2)
+    mesh, w0, out, w, W = _sharded_run(cfg, 4, 3, 0)
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    ref = g.reference_integrate(cfg.options(), 3)
+    wr, Wr, _, _ = g.get_state()
+    assert w.tobytes() == wr.tobytes() and W.tobytes() == Wr.tobytes()
+    for r in range(4):
+        assert [x["dt"] for x in out[r][0]] == [x["dt"] for x in ref]
+
+
+@pytest.mark.slow
+def test_config3_full_size_deterministic_and_physical(gpu):
+    """Config 3 at full size (8M cells, 4 levels): two runs bitwise equal,
+    density and pressure positive, records' theta and level counts sane."""
+    cfg = configs.get(3)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    outs = []
+    for _ in range(2):
+        s = Solver(mesh, "euler")
+        s.set_state(w0)
+        recs = s.reference_integrate(cfg.options(), 3)
+        outs.append((s.get_state()[0], [r["dt"] for r in recs]))
+        assert all(r["theta"] <= cfg.theta_max and sum(r["level_cells"]) == len(mesh["vol"]) for r in recs)
+        s.close()
+    assert outs[0][0].tobytes() == outs[1][0].tobytes() and outs[0][1] == outs[1][1]
+    w = outs[0][0]
+    p = 0.4 * (w[:, 4] - 0.5 * (w[:, 1] ** 2 + w[:, 2] ** 2 + w[:, 3] ** 2) / w[:, 0])
+    assert (w[:, 0] > 0).all() and (p > 0).all()
+
+
+def test_single_cell_and_isolated_cells(gpu):
+    """Edge cases of the gather kernels: a one-cell mesh (every face a
+    boundary, no neighbour: the limiter leaves the gradient alone) and a
+    2D strip; GPU == oracle bitwise."""
+    from oracle import OracleSolver
+    for nx, ny, nz in ((1, 1, 1), (5, 1, 1)):
+        mesh = meshgen.hex_mesh(meshgen.uniform_nodes(nx), meshgen.uniform_nodes(ny), meshgen.uniform_nodes(nz))
+        w0 = configs.euler_conserved(np.linspace(1.0, 2.0, nx * ny * nz), np.linspace(1.0, 3.0, nx * ny * nz))
+        g = Solver(mesh, "euler")
+        g.set_state(w0)
+        rg = g.reference_integrate(SolverOptions(2, 0.25, 1e30), 3)
+        o = OracleSolver(mesh, "euler")
+        o.init_values(w0.reshape(-1))
+        o.set_options(2, 0.25, 1e30)
+        ro = o.integrate(3)
+        assert [r["dt"] for r in rg] == [r["dt"] for r in ro]
+        np.testing.assert_array_equal(g.get_state()[0].reshape(-1), o.get("w"))
 
 
 def test_nccl_single_rank_shard(gpu):
