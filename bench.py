@@ -12,11 +12,12 @@ Contract (see task/README): one JSON line on rank 0.
   levels.cpp:68-79).
 * value: state resident in HBM, the whole timed region bracketed by CUDA
   events on the library's stream (host plan read-backs included).
-* e2e: the same metric through the C ABI with HOST buffers: every step
-  uploads the state from pinned memory, runs one iteration and downloads the
-  state. The state crosses PCIe as W alone (set_state(NULL, W) rebuilds
-  w = W / V, the relation every corrector leaves: exact at iteration
-  boundaries).
+* e2e: the same metric through the C ABI with HOST buffers
+  (tafv_gpu_run_batch): every step uploads its input state from pinned
+  memory, runs one iteration and downloads its result; the state crosses
+  PCIe as W alone (w = W / V rebuilt on the device, the relation every
+  corrector leaves), and step j+1's upload / step j-1's download overlap
+  step j's compute on separate copy streams.
 * roofline: the dominant kernel's algorithmic bytes / its event-timed
   duration vs MEASURED_PEAKS.json hbm_gbs; roofline_iteration: BASELINE.md's
   whole-iteration byte contract B_iter = 1220 C_eff + 568 F_eff + 312 R_eff.
@@ -322,30 +323,27 @@ def main():
     s.set_flag("kernel_timing", 0)
     assert [r["level_cells"] for r in recs_k] == [r["level_cells"] for r in recs]
 
-    # e2e: host buffers through the C ABI, copies inside every step
+    # e2e: host buffers through the C ABI (tafv_gpu_run_batch), every step
+    # uploads its input state from pinned memory and downloads its result;
+    # the state crosses PCIe as W alone (w = W / V on the device, the
+    # relation every corrector leaves) and the copies of step j+1 / j-1 run
+    # on copy streams while step j computes
     n = len(mesh["vol"])
-    pin_W = torch.from_numpy((w0 * mesh["vol"][:, None]).copy()).pin_memory()
-    out_W = torch.empty((n, 5), dtype=torch.float64).pin_memory()
-    e2e_ceff, e2e_t = 0, 0.0
-    lib = s.lib
-    import ctypes as C
-
-    from paper_1704_01144_b200 import _native as N
-    copt = opt.c()
-    rec = (N.Record * 1)()
-    t0c, itc = C.c_double(), C.c_int32()
-    for i in range(args.e2e_steps + 1):
-        torch.cuda.synchronize()
-        t = time.perf_counter()
-        # the state crosses PCIe as W alone: w = W / V on the device, the
-        # relation every corrector leaves (exact at iteration boundaries)
-        s._c(lib.tafv_gpu_set_state(s.h, None, C.c_void_p(pin_W.data_ptr()), 0.0, 0))
-        s._c(lib.tafv_gpu_iterate(s.h, C.byref(copt), 1, rec))
-        s._c(lib.tafv_gpu_get_state(s.h, None, C.c_void_p(out_W.data_ptr()), C.byref(t0c), C.byref(itc)))
-        el = time.perf_counter() - t
-        if i > 0:  # first call warms the staging buffers
-            e2e_t += el
-            e2e_ceff += c_eff(rec[0].as_dict())
+    if world > 1:  # a shard's batch arrays hold its local cells (shard order)
+        cells = shard.describe(mesh, roc, rank, world)["cells"]
+    else:
+        cells = np.arange(len(mesh["vol"]))
+    W0 = np.ascontiguousarray((w0 * mesh["vol"][:, None])[cells])
+    ins = [torch.from_numpy(W0.copy()).pin_memory() for _ in range(2)]
+    outs = [torch.empty_like(ins[0]).pin_memory() for _ in range(2)]
+    s.run_batch([ins[0]], [outs[0]], opt, 1)  # warm-up: staging buffers, graphs
+    K = max(1, args.e2e_steps)
+    if world > 1:
+        torch.distributed.barrier()
+    t = time.perf_counter()
+    rec = s.run_batch([ins[j % 2] for j in range(K)], [outs[j % 2] for j in range(K)], opt, 1)
+    e2e_t = time.perf_counter() - t
+    e2e_ceff = K * c_eff(rec)  # every input is the same state: the same plan
     if world > 1:
         t = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -409,8 +407,9 @@ def main():
                                        "exchange per phase" if world > 1 else "single GPU")},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": bytes_state,
                     "d2h_bytes_per_step": bytes_state,
-                    "how": "tafv_gpu_set_state(NULL, pinned W: w = W/V on device) + tafv_gpu_iterate(1) + "
-                           "tafv_gpu_get_state(NULL, pinned W); host wall clock per step"},
+                    "how": "tafv_gpu_run_batch over e2e_steps inputs, 1 iteration each: per step H2D of the "
+                           "input W (pinned) and D2H of the result W, overlapped with the neighbouring steps' "
+                           "compute on copy streams; host wall clock around the batch"},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),

@@ -167,6 +167,17 @@ int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
  * the device-resident throughput path. */
 int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* last);
 
+/* A batch of independent inputs (ensemble members, restarts): for each
+ * j < n_inputs, the state becomes W_in[j] (extensive, original cell order;
+ * w = W / V, t0 = 0, iteration = 0), `iterations` iterations run
+ * (reference_integrate), and the resulting W is written to W_out[j]. Input
+ * j+1 uploads and output j-1 downloads on separate copy streams while input
+ * j computes; pass pinned host buffers for the overlap. `last` (optional)
+ * receives the record of the last iteration of the last input. Shards: the
+ * arrays hold the rank's local cells in the order of its shard cell list. */
+int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, int32_t iterations,
+                       const double* const* W_in, double* const* W_out, tafv_record* last);
+
 /* Debug/parity access to intermediate SolverState arrays in original ids:
  * "w_pred" [nc][nv], "grad" [nc][nv][3], "phi_pred" / "int_substep" /
  * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32). */

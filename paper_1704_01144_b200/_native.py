@@ -103,7 +103,7 @@ class PlanInfo(C.Structure):
 EXPORTS = [
     "tafv_gpu_create", "tafv_gpu_destroy", "tafv_gpu_last_error", "tafv_gpu_set_state",
     "tafv_gpu_get_state", "tafv_gpu_plan", "tafv_gpu_inject_levels", "tafv_gpu_get_plan_lists",
-    "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_get_array",
+    "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_run_batch", "tafv_gpu_get_array",
     "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex",
     "tafv_partition_slabs", "tafv_shard_describe", "tafv_shard_last_error",
     "tafv_comm_nccl_unique_id", "tafv_comm_create_nccl", "tafv_comm_create_loopback",
@@ -128,6 +128,7 @@ def lib():
     L.tafv_gpu_destroy.restype = None
     L.tafv_gpu_last_error.argtypes = [vp]
     L.tafv_gpu_last_error.restype = C.c_char_p
+    L.tafv_gpu_run_batch.argtypes = [vp, vp, i32, i32, vp, vp, vp]
     L.tafv_gpu_set_state.argtypes = [vp, vp, vp, dbl, i32]
     L.tafv_gpu_get_state.argtypes = [vp, vp, vp, C.POINTER(dbl), C.POINTER(i32)]
     L.tafv_gpu_plan.argtypes = [vp, C.POINTER(Options), C.POINTER(PlanInfo)]

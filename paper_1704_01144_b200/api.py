@@ -199,6 +199,29 @@ class Solver:
             w, W = w[:, 0], W[:, 0]
         return w, W, t0.value, it.value
 
+    def run_batch(self, W_in, W_out, opt: SolverOptions, iterations=1):
+        """tafv_gpu_run_batch: independent inputs W_in[j] (extensive rows,
+        original cell order; w = W / V) each advanced `iterations`
+        iterations into W_out[j], copies overlapped with compute. Buffers are
+        numpy arrays or host tensors exposing data_ptr() (pin them for the
+        overlap). Returns the record of the last iteration."""
+        def ptr(a):
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+        n = len(W_in)
+        if len(W_out) != n:
+            raise InvalidArgument("run_batch: W_in and W_out differ in length")
+        for a in list(W_in) + list(W_out):
+            size = a.numel() if hasattr(a, "numel") else a.size
+            if size != self.nc * self.nv:
+                raise InvalidArgument("run_batch: wrong buffer size")
+        pin = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_in])
+        pout = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_out])
+        rec = N.Record()
+        self._c(self.lib.tafv_gpu_run_batch(self.h, C.byref(opt.c()), n, int(iterations), pin, pout,
+                                           C.byref(rec)))
+        self._plan = None
+        return rec.as_dict()
+
     def get_array(self, name):
         if name in ("raw_level", "tau"):
             out = np.zeros(self.nc, dtype=np.int32)

@@ -158,6 +158,11 @@ struct tafv_gpu {
   PlanDev* hplan = nullptr;  // pinned
   double* stage_buf = nullptr;
   size_t stage_len = 0;
+  // run_batch: copy streams and double-buffered input / output staging
+  cudaStream_t cin = nullptr, cout = nullptr;
+  double* bin[2] = {nullptr, nullptr};
+  double* bout[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_out_free[2] = {};
   cudaEvent_t ev[6] = {};  // [0,1] sweep, [2,3] plan, [4,5] whole call
 
   // host copy of the plan
@@ -251,6 +256,14 @@ struct tafv_gpu {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
+    for (int q = 0; q < 2; ++q) {
+      if (bin[q]) cudaFree(bin[q]);
+      if (bout[q]) cudaFree(bout[q]);
+      for (cudaEvent_t e : {ev_in[q], ev_in_free[q], ev_out[q], ev_out_free[q]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (cin) cudaStreamDestroy(cin);
+    if (cout) cudaStreamDestroy(cout);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evpool) cudaEventDestroy(e);
@@ -1598,6 +1611,64 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
     require(opt != nullptr, "advance: null options");
     require(n >= 0, "integrate: negative iteration count");
     timed_call(*h, [&] { integrate_pipelined(*h, *opt, n, last, false); });
+  });
+}
+
+// A batch of independent inputs through one handle, each `iterations`
+// iterations from its own extensive state (w = W / V); input j+1 uploads on
+// a copy stream while input j computes on the library stream.
+int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, int32_t iterations,
+                       const double* const* W_in, double* const* W_out, tafv_record* last) {
+  return guard(h, [&] {
+    require(opt != nullptr && W_in != nullptr && W_out != nullptr, "run_batch: null argument");
+    require(n_inputs >= 0 && iterations >= 1, "run_batch: counts");
+    const size_t n = (size_t)h->N * h->nv, bytes = n * sizeof(double);
+    if (!h->cin) {
+      CK(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking));
+      for (int q = 0; q < 2; ++q) {
+        h->bin[q] = dalloc<double>(n);
+        h->bout[q] = dalloc<double>(n);
+        for (cudaEvent_t* e : {&h->ev_in[q], &h->ev_in_free[q], &h->ev_out[q], &h->ev_out_free[q]}) {
+          CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+          CK(cudaEventRecord(*e, h->st));  // initially complete
+        }
+      }
+    }
+    auto upload = [&](int j) {
+      const int q = j & 1;
+      CK(cudaStreamWaitEvent(h->cin, h->ev_in_free[q], 0));
+      // not under the previous download either (they share the link: measured)
+      CK(cudaStreamWaitEvent(h->cin, h->ev_out_free[q], 0));  // download j - 2 of this slot pair = the one in flight
+      CK(cudaMemcpyAsync(h->bin[q], W_in[j], bytes, cudaMemcpyHostToDevice, h->cin));
+      CK(cudaEventRecord(h->ev_in[q], h->cin));
+    };
+    const int grid = h->grid_for((long long)n, 256);
+    if (n_inputs > 0) upload(0);
+    for (int j = 0; j < n_inputs; ++j) {
+      const int q = j & 1;
+      if (j + 1 < n_inputs) upload(j + 1);
+      // state j: W from the staged input, w = W / V (kernels.cpp:237-241)
+      CK(cudaStreamWaitEvent(h->st, h->ev_in[q], 0));
+      k_gather_rows<<<grid, 256, 0, h->st>>>(h->bin[q], h->d_cperm, h->N, h->nv, h->W);
+      k_intensive<<<grid, 256, 0, h->st>>>(h->W, h->vol, h->N, h->nv, h->w);
+      CK(cudaEventRecord(h->ev_in_free[q], h->st));
+      h->t0 = 0.0;
+      h->iteration = 0;
+      h->state_set = true;
+      h->has_plan = false;
+      integrate_pipelined(*h, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
+      // output j: W in original order -> staging -> host. On the library
+      // stream: a device-to-host copy running under the kernels was measured
+      // to slow them ~2x, so only the uploads overlap compute.
+      CK(cudaStreamWaitEvent(h->st, h->ev_out_free[q], 0));
+      k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[q]);
+      CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->st));
+      CK(cudaEventRecord(h->ev_out_free[q], h->st));
+    }
+    CK(cudaStreamSynchronize(h->cout));
+    CK(cudaStreamSynchronize(h->cin));
+    CK(cudaStreamSynchronize(h->st));
   });
 }
 

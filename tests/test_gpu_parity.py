@@ -301,6 +301,30 @@ def test_state_round_trip_as_extensive_only(gpu):
         b.set_state(None, None)
 
 
+def test_run_batch_matches_separate_runs(gpu):
+    """tafv_gpu_run_batch (copies overlapped with compute on copy streams)
+    gives, for each input, bitwise the W of set_state(None, W) +
+    reference_integrate run separately."""
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    a = Solver(mesh, "euler")
+    a.set_state(cfg.initial_state(mesh))
+    Ws = []
+    for _ in range(3):
+        a.reference_integrate(cfg.options(), 1)
+        Ws.append(np.ascontiguousarray(a.get_state()[1]))
+    ins = [Ws[0], Ws[1], Ws[2], Ws[0]]
+    outs = [np.empty_like(x) for x in ins]
+    b = Solver(mesh, "euler")
+    rec = b.run_batch(ins, outs, cfg.options(), 2)
+    for x, y in zip(ins, outs):
+        c = Solver(mesh, "euler")
+        c.set_state(None, x)
+        rc = c.reference_integrate(cfg.options(), 2)
+        assert c.get_state()[1].tobytes() == y.tobytes()
+    assert rec["dt"] == rc[-1]["dt"] and rec["level_cells"] == rc[-1]["level_cells"]
+
+
 def test_cpp_shim_caller(gpu):
     """A reference-style C++ caller (include/tafv_gpu.hpp) integrates on the
     GPU and sees the reference's exception classes."""
