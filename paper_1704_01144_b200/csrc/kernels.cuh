@@ -877,6 +877,19 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(CompactJobs jo
   }
 }
 
+// The one-graph iteration's switch: theta of the plan just made (max level
+// with cells), or past the last case (no sweep) when plan_iteration would
+// have thrown (level error, non-finite or non-positive stable step).
+__global__ void k_select_sweep(const PlanDev* plan, cudaGraphConditionalHandle h, int theta_max) {
+  if (threadIdx.x != 0) return;
+  int th = 0;
+  for (int l = 0; l < kMaxLevels; ++l)
+    if (plan->gcell_count[l] > 0) th = l;
+  const double dt = plan->dt_min;
+  const bool ok = plan->err == 0 && isfinite(dt) && dt > 0.0;
+  cudaGraphSetConditional(h, ok ? (unsigned)th : (unsigned)theta_max + 1);
+}
+
 // Halo rows: pack owned rows for the peers, unpack received halo rows.
 __global__ void k_pack_rows(const double* src, const int* idx, int n, int width, double* dst) {
   const size_t total = (size_t)n * width;

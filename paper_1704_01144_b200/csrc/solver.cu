@@ -163,6 +163,11 @@ struct tafv_gpu {
   double* bin[2] = {nullptr, nullptr};
   double* bout[2] = {nullptr, nullptr};
   cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_out_free[2] = {};
+  // one-graph iteration (build_iter_graph) and its per-iteration plan copies
+  cudaGraphExec_t iter_graph = nullptr;
+  cudaGraphConditionalHandle iter_cond{};
+  tafv_options iter_opt{};
+  std::vector<PlanDev> batch_plans;
   cudaEvent_t ev[6] = {};  // [0,1] sweep, [2,3] plan, [4,5] whole call
 
   // host copy of the plan
@@ -247,6 +252,7 @@ struct tafv_gpu {
       for (auto e : g.second.evs) cudaEventDestroy(e);
     }
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
+    if (iter_graph) cudaGraphExecDestroy(iter_graph);
     void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
@@ -837,6 +843,8 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
 }
 
 // Host side of the plan once its read-back landed (after a stream sync).
+void parse_plan(tafv_gpu& h);
+
 void accept_plan(tafv_gpu& h) {
   {
     float ms = 0.f;
@@ -847,6 +855,11 @@ void accept_plan(tafv_gpu& h) {
       h.kcnt[tafv_gpu::kPlan] += 1;
     }
   }
+  parse_plan(h);
+}
+
+// The host copy of a plan (h.hplan) -> levels, counts, dt; error flags throw.
+void parse_plan(tafv_gpu& h) {
   const PlanDev& p = *h.hplan;
   const int nkeys = h.plan_nkeys;
   h.has_plan = false;
@@ -1614,6 +1627,56 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
   });
 }
 
+// One whole iteration as ONE graph (single domain): the plan graph's
+// kernels, a selector kernel that sets a switch condition to theta (or past
+// the last case when the plan failed: stable step collapsed / level error),
+// and a SWITCH node whose case theta is the captured sweep of that theta. No
+// host round trip between plan and sweep.
+void build_iter_graph(tafv_gpu& h, const tafv_options& opt) {
+  if (h.iter_graph) CK(cudaGraphExecDestroy(h.iter_graph));
+  h.iter_graph = nullptr;
+  cudaGraph_t g;
+  CK(cudaGraphCreate(&g, 0));
+  CK(cudaGraphConditionalHandleCreate(&h.iter_cond, g, (unsigned)opt.theta_max + 1, cudaGraphCondAssignDefault));
+  const int64_t l0 = h.launches;
+  const int theta0 = h.theta;
+  h.capturing = true;
+  CK(cudaStreamBeginCaptureToGraph(h.st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  plan_kernels(h, opt);
+  k_select_sweep<<<1, 32, 0, h.st>>>(h.dplan, h.iter_cond, opt.theta_max);
+  CK(cudaStreamEndCapture(h.st, &g));
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn), leaves;
+  CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+  for (cudaGraphNode_t nd : nodes) {
+    size_t nd_out = 0;
+    CK(cudaGraphNodeGetDependentNodes(nd, nullptr, &nd_out));
+    if (nd_out == 0) leaves.push_back(nd);
+  }
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h.iter_cond;
+  cp.conditional.type = cudaGraphCondTypeSwitch;
+  cp.conditional.size = (unsigned)opt.theta_max + 1;
+  cudaGraphNode_t cn;
+  CK(cudaGraphAddNode(&cn, g, leaves.data(), leaves.size(), &cp));
+  for (int th = 0; th <= opt.theta_max; ++th) {
+    h.theta = th;  // the sweep's level sequence; counts come from the device plan
+    CK(cudaStreamBeginCaptureToGraph(h.st, cp.conditional.phGraph_out[th], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    enqueue_sweep_direct(h);
+    cudaGraph_t body;
+    CK(cudaStreamEndCapture(h.st, &body));
+  }
+  h.capturing = false;
+  h.theta = theta0;
+  CK(cudaGraphInstantiate(&h.iter_graph, g, 0));
+  CK(cudaGraphDestroy(g));
+  h.iter_opt = opt;
+  h.launches = l0;
+}
+
 // A batch of independent inputs through one handle, each `iterations`
 // iterations from its own extensive state (w = W / V); input j+1 uploads on
 // a copy stream while input j computes on the library stream.
@@ -1644,6 +1707,15 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
       CK(cudaEventRecord(h->ev_in[q], h->cin));
     };
     const int grid = h->grid_for((long long)n, 256);
+    // single domain: every iteration is one graph launch (plan + switch to
+    // the sweep of its theta), no host synchronisation inside the batch
+    const bool one_graph = !h->sharded() && h->use_graph && h->plan_graph_on && !h->ktime;
+    if (one_graph) {
+      const bool same = h->iter_graph && h->iter_opt.theta_max == opt->theta_max &&
+                        h->iter_opt.cfl == opt->cfl && h->iter_opt.dt_cap == opt->dt_cap;
+      if (!same) build_iter_graph(*h, *opt);
+      h->batch_plans.resize((size_t)n_inputs * iterations);
+    }
     if (n_inputs > 0) upload(0);
     for (int j = 0; j < n_inputs; ++j) {
       const int q = j & 1;
@@ -1657,7 +1729,16 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
       h->iteration = 0;
       h->state_set = true;
       h->has_plan = false;
-      integrate_pipelined(*h, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
+      if (one_graph) {
+        for (int it = 0; it < iterations; ++it) {
+          CK(cudaGraphLaunch(h->iter_graph, h->st));
+          // this iteration's plan + its sweep's flags and totals
+          CK(cudaMemcpyAsync(&h->batch_plans[(size_t)j * iterations + it], h->dplan, sizeof(PlanDev),
+                             cudaMemcpyDeviceToHost, h->st));
+        }
+      } else {
+        integrate_pipelined(*h, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
+      }
       // output j: W in original order -> staging -> host. On the library
       // stream: a device-to-host copy running under the kernels was measured
       // to slow them ~2x, so only the uploads overlap compute.
@@ -1669,6 +1750,23 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
     CK(cudaStreamSynchronize(h->cout));
     CK(cudaStreamSynchronize(h->cin));
     CK(cudaStreamSynchronize(h->st));
+    if (one_graph) {  // the plans and flags of every iteration, in order
+      for (int j = 0; j < n_inputs; ++j) {
+        h->t0 = 0.0;
+        h->iteration = 0;
+        for (int it = 0; it < iterations; ++it) {
+          *h->hplan = h->batch_plans[(size_t)j * iterations + it];
+          h->plan_nkeys = opt->theta_max + 1;
+          parse_plan(*h);
+          if (!(std::isfinite(h->dt) && h->dt > 0.0)) {
+            h->has_plan = false;
+            throw Error{TAFV_EINVAL, "integrate: stable step collapsed"};
+          }
+          close_iteration(*h, j + 1 == n_inputs && it + 1 == iterations ? last : nullptr);
+        }
+      }
+      h->has_plan = false;
+    }
   });
 }
 

@@ -323,6 +323,18 @@ def test_run_batch_matches_separate_runs(gpu):
         rc = c.reference_integrate(cfg.options(), 2)
         assert c.get_state()[1].tobytes() == y.tobytes()
     assert rec["dt"] == rc[-1]["dt"] and rec["level_cells"] == rc[-1]["level_cells"]
+    assert rec["total_extensive"] == rc[-1]["total_extensive"] and rec["t_start"] == rc[-1]["t_start"]
+    # the direct-launch path (no one-graph iteration) agrees
+    d = Solver(mesh, "euler")
+    d.set_flag("use_graph", 0)
+    outs2 = [np.empty_like(x) for x in ins]
+    d.run_batch(ins, outs2, cfg.options(), 2)
+    assert all(x.tobytes() == y.tobytes() for x, y in zip(outs, outs2))
+    # a diverging input surfaces as the reference's runtime_error
+    bad = Ws[0].copy()
+    bad[: len(bad) // 2, 4] = -1.0
+    with pytest.raises((Diverged, InvalidArgument)):
+        b.run_batch([Ws[1], bad], [np.empty_like(bad), np.empty_like(bad)], cfg.options(), 2)
 
 
 def test_cpp_shim_caller(gpu):
