@@ -176,8 +176,7 @@ def reference_library_scalar2d(threads, iterations=2):
         from oracle import RefSolver, ref_available, ref_generate_mesh
         if not ref_available():
             return {"unavailable": "oracle/_ref/libtafv_ref.so not built"}
-        _, _, mh = ref_generate_mesh(dim=2, nx=800, ny=800, periodic_x=True, periodic_y=True,
-                                     regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+        _, _, mh = ref_generate_mesh(**SCALAR2D_SPEC)
         out = {"workload": "scalar 2D advection, 800x800 torus + 2x block (reference generate_mesh)",
                "unit": UNIT}
         for leg in ("sequential", "task_engine"):
@@ -195,6 +194,40 @@ def reference_library_scalar2d(threads, iterations=2):
                         "cores": 1 if leg == "sequential" else threads}
         return out
     except Exception as e:  # context field only; never fails the arm
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
+SCALAR2D_SPEC = dict(dim=2, nx=800, ny=800, periodic_x=True, periodic_y=True,
+                     regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+
+
+def gpu_scalar2d_reference_workload(iterations=10):
+    """Our library on the reference library's OWN workload (scalar 2D
+    advection on the reference generate_mesh 800x800 torus + 2x block,
+    1.12M cells, the same initial state and options as
+    reference_library_scalar2d): a like-for-like comparison with the
+    reference's sequential and task-parallel CPU paths."""
+    try:
+        from oracle import RefSolver, ref_available, ref_generate_mesh
+        if not ref_available():
+            return {"unavailable": "oracle/_ref/libtafv_ref.so not built"}
+        from paper_1704_01144_b200 import Solver, SolverOptions
+        mesh, _, mh = ref_generate_mesh(**SCALAR2D_SPEC)
+        r = RefSolver(mh, "advection", (1.0, 0.5))
+        r.init_gaussian(sigma=0.15)
+        w0 = r.get("w").copy()
+        g = Solver(mesh, "advection", (1.0, 0.5))
+        g.set_state(w0)
+        opt = SolverOptions(3, 0.5, 1.0)
+        g.reference_integrate(opt, 2)
+        recs = g.reference_integrate(opt, iterations)
+        ms = g.stats()["ms_total"]
+        g.close()
+        return {"workload": "scalar 2D advection, reference generate_mesh 800x800 torus + 2x block",
+                "cells": int(len(mesh["vol"])), "iterations": iterations,
+                "value": sum(c_eff(x) for x in recs) / (ms / 1e3), "unit": UNIT,
+                "compare": "bench.py --impl reference: reference_library_scalar2d"}
+    except Exception as e:  # context field only
         return {"unavailable": f"{type(e).__name__}: {e}"}
 
 
@@ -427,6 +460,8 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
+        if world == 1:
+            line["scalar2d_reference_workload"] = gpu_scalar2d_reference_workload()
         print(json.dumps(line), flush=True)
     s.close()
     if comm is not None:

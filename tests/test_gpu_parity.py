@@ -411,6 +411,30 @@ def test_sharded_loopback_matches_single_domain_bitwise(cid, scale, world, iters
 
 
 @pytest.mark.slow
+def test_reference_library_workload_full_size_bitwise(gpu):
+    """The reference library's own workload at the bench's N-matched size
+    (reference generate_mesh 800x800 torus + 2x block, 1.12M cells, scalar
+    advection): GPU == the UNMODIFIED reference (oracle/_ref) bitwise after
+    3 iterations, records included."""
+    from oracle import RefSolver, ref_available, ref_generate_mesh
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    mesh, _, mh = ref_generate_mesh(dim=2, nx=800, ny=800, periodic_x=True, periodic_y=True,
+                                    regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+    r = RefSolver(mh, "advection", (1.0, 0.5))
+    r.init_gaussian(sigma=0.15)
+    r.set_options(3, 0.5, 1.0)
+    g = Solver(mesh, "advection", (1.0, 0.5))
+    g.set_state(r.get("w").copy())
+    rg = g.reference_integrate(SolverOptions(3, 0.5, 1.0), 3)
+    rr = r.integrate(3)
+    assert [x["dt"] for x in rg] == [x["dt"] for x in rr]
+    assert [x["level_cells"] for x in rg] == [x["level_cells"] for x in rr]
+    w, W, _, _ = g.get_state()
+    assert w.tobytes() == r.get("w").tobytes() and W.tobytes() == r.get("W").tobytes()
+
+
+@pytest.mark.slow
 def test_sharded_full_size_config2_bitwise(gpu):
     """Config 2 at its full size (1M cells) as 4 slab shards: bitwise the
     single-domain run (a size-independent decomposition invariant)."""
