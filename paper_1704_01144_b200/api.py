@@ -201,7 +201,8 @@ class Solver:
 
     def run_batch(self, W_in, W_out, opt: SolverOptions, iterations=1):
         """tafv_gpu_run_batch: independent inputs W_in[j] (extensive rows,
-        original cell order; w = W / V) each advanced `iterations`
+        original cell order -- a shard: its local cells in
+        shard.describe()["cells"] order; w = W / V) each advanced `iterations`
         iterations into W_out[j], copies overlapped with compute. Buffers are
         numpy arrays or host tensors exposing data_ptr() (pin them for the
         overlap). Returns the record of the last iteration."""
@@ -210,9 +211,11 @@ class Solver:
         n = len(W_in)
         if len(W_out) != n:
             raise InvalidArgument("run_batch: W_in and W_out differ in length")
+        # a shard's arrays hold its local cells (shard.describe()["cells"] order)
+        rows = self.mesh_info()["n_cells"] if hasattr(self, "rank") else self.nc
         for a in list(W_in) + list(W_out):
             size = a.numel() if hasattr(a, "numel") else a.size
-            if size != self.nc * self.nv:
+            if size != rows * self.nv:
                 raise InvalidArgument("run_batch: wrong buffer size")
         pin = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_in])
         pout = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_out])

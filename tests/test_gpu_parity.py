@@ -337,6 +337,50 @@ def test_run_batch_matches_separate_runs(gpu):
         b.run_batch([Ws[1], bad], [np.empty_like(bad), np.empty_like(bad)], cfg.options(), 2)
 
 
+def test_run_batch_sharded_loopback(gpu):
+    """run_batch on 2 loopback shards (local arrays in shard order): the
+    owned rows equal the single-domain batch bitwise."""
+    import threading
+
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    W0 = cfg.initial_state(mesh) * mesh["vol"][:, None]
+    single = Solver(mesh, "euler")
+    ref = [np.empty_like(W0) for _ in range(2)]
+    single.run_batch([W0, W0], ref, cfg.options(), 2)
+    roc = shard.partition_slabs(mesh, 2, axis=0)
+    comm = Comm.loopback(2)
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(2)]
+    descs = [shard.describe(mesh, roc, r, 2) for r in range(2)]
+    outs, errs = {}, []
+
+    def body(r):
+        try:
+            cells = descs[r]["cells"]
+            ins = [np.ascontiguousarray(W0[cells]) for _ in range(2)]
+            o = [np.empty_like(x) for x in ins]
+            solvers[r].run_batch(ins, o, cfg.options(), 2)
+            outs[r] = o
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for s_ in solvers:
+        s_.close()
+    comm.close()
+    assert not errs, errs
+    for r in range(2):
+        cells, own = descs[r]["cells"], descs[r]["cls"] == 0
+        for j in range(2):
+            assert outs[r][j][own].tobytes() == ref[j][cells[own]].tobytes()
+
+
 def test_cpp_shim_caller(gpu):
     """A reference-style C++ caller (include/tafv_gpu.hpp) integrates on the
     GPU and sees the reference's exception classes."""
