@@ -158,6 +158,15 @@ template <int NV>
 struct GradRow {
   static constexpr int S = (NV * 3 + 3) / 4 * 4;
 };
+// Face integral rows (phi_pred, int_substep, int_window) padded to an even
+// number of doubles (Euler: 5 -> 6, 48 B) for 128-bit stores / loads.
+template <int NV>
+struct FaceRow {
+  static constexpr int S = (NV + 1) / 2 * 2;
+};
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
 
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
 __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
@@ -402,26 +411,42 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     }
     double r[NV];
     rusanov<P>(pp, wL, wR, nrm, r);
-    double* phi = s.phi + (size_t)f * NV;
-    double* iwin = s.iwin + (size_t)f * NV;
+    constexpr int FS = FaceRow<NV>::S;
+    double* phi = s.phi + (size_t)f * FS;
+    double* iwin = s.iwin + (size_t)f * FS;
     if (PRED) {
+      double row[FS];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) phi[k] = r[k] * gm.w;
+      for (int k = 0; k < FS; ++k) row[k] = k < NV ? r[k] * gm.w : 0.0;
+#pragma unroll
+      for (int q = 0; q < FS; q += 2) st2(phi + q, row[q], row[q + 1]);
       if (shared_start && !(eq && s.ialias)) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) iwin[k] = 0.0;
       }
     } else {
       const double dt_sub = dt * (double)(1 << s.cad[f]);
-      double* isub = s.isub + (size_t)f * NV;
+      double* isub = s.isub + (size_t)f * FS;
       const bool skip = eq && s.ialias;
+      double row[FS];
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const double phi_corr = r[k] * gm.w;
-        const double v = 0.5 * dt_sub * (phi[k] + phi_corr);
-        isub[k] = v;
-        if (!skip) iwin[k] = iwin[k] + v;
+      for (int q = 0; q < FS; q += 2) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(phi + q));
+        row[q] = v.x;
+        row[q + 1] = v.y;
       }
+#pragma unroll
+      for (int k = 0; k < FS; ++k) {
+        if (k < NV) {
+          const double phi_corr = r[k] * gm.w;
+          row[k] = 0.5 * dt_sub * (row[k] + phi_corr);
+          if (!skip) iwin[k] = iwin[k] + row[k];
+        } else {
+          row[k] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < FS; q += 2) st2(isub + q, row[q], row[q + 1]);
       if (s.ialias) s.ialias[f] = skip ? 1 : 0;
     }
   }
@@ -487,7 +512,7 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
         const double* ph;
         if (PRED) ph = s.phi;
         else ph = tc > s.cad[f] ? s.iwin : s.isub;
-        sum += slot_sign(e) * ph[(size_t)f * NV + k];
+        sum += slot_sign(e) * ph[(size_t)f * FaceRow<NV>::S + k];
       }
       const size_t ci = (size_t)c * NV + k;
       const double v = m.vol[c];
@@ -926,11 +951,13 @@ __global__ void k_gather_rows(const double* src, const int* perm, int n, int wid
 // value the reference's reset-then-accumulate leaves (kernels.cpp:123-130,
 // 183-185).
 __global__ void k_window_rows(const double* iwin, const double* isub, const uint8_t* alias, int n,
-                              int width, double* dst) {
+                              int width, int stride, double* dst) {
   const long long total = (long long)n * width;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[i] = alias[i / width] ? isub[i] + 0.0 : iwin[i];
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / width, j = row * stride + i % width;
+    dst[i] = alias[row] ? isub[j] + 0.0 : iwin[j];
+  }
 }
 
 __global__ void k_scatter_rows(const double* src, const int* perm, int n, int width, double* dst) {

@@ -141,6 +141,7 @@ struct tafv_gpu {
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
   size_t gs = 0;  // gradient row stride in doubles (padded, see GradRow)
+  size_t fs = 0;  // face-integral row stride in doubles (padded, see FaceRow)
   double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
   uint8_t* ialias = nullptr;  // [F] see StateDev::ialias
   bool iwin_alias = true;
@@ -610,16 +611,17 @@ void alloc_state(tafv_gpu& h) {
   h.wp = dalloc<double>(N * nv);
   h.gs = (nv * 3 + 3) / 4 * 4;  // GradRow<NV>::S
   h.grad = dalloc<double>(N * h.gs);
-  h.phi = dalloc<double>(F * nv);
-  h.isub = dalloc<double>(F * nv);
-  h.iwin = dalloc<double>(F * nv);
+  h.fs = (nv + 1) / 2 * 2;  // FaceRow<NV>::S
+  h.phi = dalloc<double>(F * h.fs);
+  h.isub = dalloc<double>(F * h.fs);
+  h.iwin = dalloc<double>(F * h.fs);
   CK(cudaMemset(h.w, 0, N * nv * sizeof(double)));
   CK(cudaMemset(h.W, 0, N * nv * sizeof(double)));
   CK(cudaMemset(h.wp, 0, N * nv * sizeof(double)));
   CK(cudaMemset(h.grad, 0, N * h.gs * sizeof(double)));
-  CK(cudaMemset(h.phi, 0, F * nv * sizeof(double)));
-  CK(cudaMemset(h.isub, 0, F * nv * sizeof(double)));
-  CK(cudaMemset(h.iwin, 0, F * nv * sizeof(double)));
+  CK(cudaMemset(h.phi, 0, F * h.fs * sizeof(double)));
+  CK(cudaMemset(h.isub, 0, F * h.fs * sizeof(double)));
+  CK(cudaMemset(h.iwin, 0, F * h.fs * sizeof(double)));
   h.ialias = dalloc<uint8_t>(F);
   CK(cudaMemset(h.ialias, 0, F));
   h.tau = dalloc<int8_t>(N);
@@ -1793,12 +1795,17 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
       cudaFree(dense);
     }
     else if (n == "dt_max") rows(h->dtmax, h->N, 1, h->d_cperm);
-    else if (n == "phi_pred") rows(h->phi, h->F, h->nv, h->d_fperm);
-    else if (n == "int_substep") rows(h->isub, h->F, h->nv, h->d_fperm);
+    else if (n == "phi_pred" || n == "int_substep") {  // padded rows -> nv wide
+      double* dense = dalloc<double>((size_t)h->F * h->nv);
+      CK(cudaMemcpy2DAsync(dense, h->nv * sizeof(double), n == "phi_pred" ? h->phi : h->isub,
+                           h->fs * sizeof(double), h->nv * sizeof(double), h->F, cudaMemcpyDeviceToDevice, h->st));
+      rows(dense, h->F, h->nv, h->d_fperm);
+      cudaFree(dense);
+    }
     else if (n == "int_window") {
       double* win = dalloc<double>((size_t)h->F * h->nv);
       k_window_rows<<<h->grid_for((long long)h->F * h->nv, 256), 256, 0, h->st>>>(h->iwin, h->isub, h->ialias,
-                                                                             h->F, h->nv, win);
+                                                                             h->F, h->nv, (int)h->fs, win);
       rows(win, h->F, h->nv, h->d_fperm);
       cudaFree(win);
     }
