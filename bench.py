@@ -92,7 +92,7 @@ class ClockSampler:
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device=0, period=0.005):
+    def __init__(self, device=0, period=0.002):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period = period
         try:
@@ -125,6 +125,9 @@ class ClockSampler:
         if self.ok:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()  # the sampler is live before the timed region starts
+            while not self.samples and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.0005)
         return self
 
     def __exit__(self, *a):
