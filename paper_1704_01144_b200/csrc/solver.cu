@@ -168,7 +168,8 @@ struct tafv_gpu {
   cudaGraphExec_t iter_graph = nullptr;
   cudaGraphConditionalHandle iter_cond{};
   tafv_options iter_opt{};
-  std::vector<PlanDev> batch_plans;
+  PlanDev* batch_plans = nullptr;  // pinned: the copies stay asynchronous
+  size_t batch_cap = 0;
   cudaEvent_t ev[6] = {};  // [0,1] sweep, [2,3] plan, [4,5] whole call
 
   // host copy of the plan
@@ -253,6 +254,7 @@ struct tafv_gpu {
       for (auto e : g.second.evs) cudaEventDestroy(e);
     }
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
+    if (batch_plans) cudaFreeHost(batch_plans);
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
@@ -1716,7 +1718,12 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
       const bool same = h->iter_graph && h->iter_opt.theta_max == opt->theta_max &&
                         h->iter_opt.cfl == opt->cfl && h->iter_opt.dt_cap == opt->dt_cap;
       if (!same) build_iter_graph(*h, *opt);
-      h->batch_plans.resize((size_t)n_inputs * iterations);
+      const size_t need = (size_t)n_inputs * iterations;
+      if (need > h->batch_cap) {
+        if (h->batch_plans) CK(cudaFreeHost(h->batch_plans));
+        CK(cudaMallocHost(&h->batch_plans, need * sizeof(PlanDev)));
+        h->batch_cap = need;
+      }
     }
     if (n_inputs > 0) upload(0);
     for (int j = 0; j < n_inputs; ++j) {
