@@ -89,8 +89,12 @@ struct PlanDev {
   double totals[8];     // sum of W per component after the last iteration
   int ncell_prefix[kMaxLevels];  // |{c owned : tau_c <= l}|: K3 active cells of level l
   int nface_prefix[kMaxLevels];  // |{f touching owned : cadence_f <= l}|: K2 active faces
-  int nk1_prefix[kMaxLevels];    // |{c owned or ring 1 : tau_c <= l}|: K1 active cells
-  long long k1_count[kMaxLevels];    // per-level counts of the K1 list (owned + ring 1)
+  // K1 active cells. Single domain: the K3 list. Shards: two lists, so the
+  // cells that read no halo row run while the halo exchange is in flight:
+  int nk1_prefix[kMaxLevels];    // |{c owned, no halo neighbour : tau_c <= l}| ("deep")
+  int nkb_prefix[kMaxLevels];    // |{c owned with a halo neighbour, or ring 1 : tau_c <= l}| ("border")
+  long long k1_count[kMaxLevels];    // per-level counts of the deep K1 list
+  long long kb_count[kMaxLevels];    // per-level counts of the border K1 list
   long long gcell_count[kMaxLevels]; // owned counts summed over ranks (records, theta)
 };
 
@@ -203,7 +207,7 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
 template <class P, int DEG>
 __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, StateDev s,
                                                     const int* __restrict__ list,
-                                                    const int* __restrict__ n_dev, int front,
+                                                    const int* __restrict__ n_dev, int base, int front,
                                                     int pred, int rev) {
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
     // rev: walk the items backwards, so this kernel starts on the rows its
     // predecessor wrote last (still in L2); consecutive kernels alternate.
     const int i = rev ? n - 1 - ii : ii;
-    const int c = list ? list[i] : i;
+    const int c = list ? list[i] : base + i;
     double we[NV];
     stage_spec<NV>(s, c, front, pred, we);
     double g[NV][D];
@@ -799,12 +803,13 @@ struct CompactJob {
   const int8_t* key;
   int n, ntiles;
   int* counts;       // [nkeys][ntiles]: counts in, exclusive offsets out
-  int* list;
+  int* list;         // item ids base + i (key points at item `base`)
   long long* totals; // [kMaxLevels]
   int* prefix;       // [kMaxLevels]
+  int base;
 };
 struct CompactJobs {
-  CompactJob j[3];
+  CompactJob j[4];
   int njobs;
 };
 
@@ -890,7 +895,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(CompactJobs jo
     if (k >= 0) {
       int pos = running[k] + rank;
       for (int w = 0; w < warp; ++w) pos += wcount[w][k];
-      jb.list[pos] = i;
+      jb.list[pos] = jb.base + i;
     }
     __syncthreads();
     if (threadIdx.x < nkeys) {

@@ -191,10 +191,11 @@ struct tafv_gpu {
   int64_t kcnt[kNumKinds] = {};
   int64_t kitems[kNumKinds][3] = {};  // active cells, active faces, fringe cells per kind
 
-  // multi-GPU shard. Internal cells [0, n_own) are owned,
-  // [n_own, n_k1) ring 1, [n_k1, N) ring 2; faces [0, F_own) touch an owned
-  // cell. Single domain: n_own = n_k1 = N, F_own = F, no comm.
-  int rank = 0, nranks = 1, n_own = 0, n_k1 = 0, F_own = 0, N_global = 0;
+  // multi-GPU shard. Internal cells [0, n_deep) are owned
+  // cells with no halo neighbour, [n_deep, n_own) owned cells next to the
+  // halo, [n_own, n_k1) ring 1, [n_k1, N) ring 2; faces [0, F_own) touch an
+  // owned cell. Single domain: n_deep = n_own = n_k1 = N, F_own = F, no comm.
+  int rank = 0, nranks = 1, n_deep = 0, n_own = 0, n_k1 = 0, F_own = 0, N_global = 0;
   tafv_comm* comm = nullptr;
   std::vector<int> shard_cells;  // local original id -> global cell id
   struct Peer {
@@ -204,9 +205,17 @@ struct tafv_gpu {
   int *d_send_idx = nullptr, *d_recv_idx = nullptr;
   int send_total = 0, recv_total = 0;
   double *sendbuf = nullptr, *recvbuf = nullptr;
-  int* klist = nullptr;       // K1 list (owned + ring 1); == clist when single domain
+  int* klist = nullptr;       // K1 list of the deep cells; == clist when single domain
+  int* kblist = nullptr;      // K1 list of the border cells (owned next to the halo + ring 1)
   int* k1_counts = nullptr;
-  int ntile_k = 0;
+  int* kb_counts = nullptr;
+  int ntile_k = 0, ntile_kb = 0;
+  // Halo exchange overlap: the rows a K3 just wrote leave on the comm stream
+  // (`cst`, high priority) while the next phase's K1 runs over the deep
+  // cells on `st`; `st` joins `ev_halo` before the border cells.
+  cudaStream_t cst = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+  bool halo_pending = false;
   long long gcount[kMaxLevels] = {};  // owned counts over all ranks
   bool sharded() const { return comm != nullptr; }
   // traversal direction of the next hot kernel (alternating, see k_grad_limit)
@@ -261,7 +270,7 @@ struct tafv_gpu {
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
-                    klist != clist ? klist : nullptr, k1_counts};
+                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
@@ -277,9 +286,19 @@ struct tafv_gpu {
       if (e) cudaEventDestroy(e);
     for (auto& e : evpool) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
+    if (cst) cudaStreamDestroy(cst);
+    if (ev_pack) cudaEventDestroy(ev_pack);
+    if (ev_halo) cudaEventDestroy(ev_halo);
   }
 };
 
+
+// The compute stream waits for the halo rows in flight on the comm stream.
+void halo_join(tafv_gpu& h) {
+  if (!h.halo_pending) return;
+  CK(cudaStreamWaitEvent(h.st, h.ev_halo, 0));
+  h.halo_pending = false;
+}
 
 // ---- transports (comm.h) ------------------------------------------------------
 namespace {
@@ -314,14 +333,14 @@ struct NcclComm final : tafv_comm {
   void allreduce_sum_i64(int, long long* d, int n, cudaStream_t st) override {
     NK(ncclAllReduce(d, d, n, ncclInt64, ncclSum, c, st));
   }
-  void exchange(tafv_gpu& h, int bpr) override {
+  void exchange(tafv_gpu& h, int bpr, cudaStream_t st) override {
     // grouped send/recv with every peer (the slab neighbours), one launch
     NK(ncclGroupStart());
     for (const auto& p : h.peers) {
       char* sb = reinterpret_cast<char*>(h.sendbuf) + (size_t)p.soff * bpr;
       char* rb = reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr;
-      if (p.nsend) NK(ncclSend(sb, (size_t)p.nsend * bpr, ncclChar, p.rank, c, h.st));
-      if (p.nrecv) NK(ncclRecv(rb, (size_t)p.nrecv * bpr, ncclChar, p.rank, c, h.st));
+      if (p.nsend) NK(ncclSend(sb, (size_t)p.nsend * bpr, ncclChar, p.rank, c, st));
+      if (p.nrecv) NK(ncclRecv(rb, (size_t)p.nrecv * bpr, ncclChar, p.rank, c, st));
     }
     NK(ncclGroupEnd());
   }
@@ -378,8 +397,8 @@ struct LoopbackComm final : tafv_comm {
   void allreduce_sum_i64(int rank, long long* d, int n, cudaStream_t st) override {
     allreduce(i64, rank, d, n, st, [](long long a, long long b) { return a + b; });
   }
-  void exchange(tafv_gpu& h, int bpr) override {
-    CK(cudaStreamSynchronize(h.st));  // my packed rows are in sendbuf
+  void exchange(tafv_gpu& h, int bpr, cudaStream_t st) override {
+    CK(cudaStreamSynchronize(st));  // my packed rows are in sendbuf
     barrier();
     for (const auto& p : h.peers) {
       const tafv_gpu& g = *members[p.rank];
@@ -390,9 +409,9 @@ struct LoopbackComm final : tafv_comm {
       if (p.nrecv)
         CK(cudaMemcpyAsync(reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr,
                            reinterpret_cast<const char*>(g.sendbuf) + (size_t)back->soff * bpr,
-                           (size_t)p.nrecv * bpr, cudaMemcpyDeviceToDevice, h.st));
+                           (size_t)p.nrecv * bpr, cudaMemcpyDeviceToDevice, st));
     }
-    CK(cudaStreamSynchronize(h.st));  // peers may reuse their send buffers
+    CK(cudaStreamSynchronize(st));  // peers may reuse their send buffers
     barrier();
   }
 };
@@ -435,7 +454,22 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
       lo[d] = std::min(lo[d], mv.cell_centroid[3 * (size_t)c + d]);
       hi[d] = std::max(hi[d], mv.cell_centroid[3 * (size_t)c + d]);
     }
-  // (ring class, Morton, id): owned cells first, then ring 1, then ring 2.
+  // (class, Morton, id): owned cells first -- those with no halo neighbour
+  // ("deep", K1 runs on them while the halo exchange is in flight), then
+  // those next to the halo -- then ring 1, then ring 2.
+  std::vector<uint8_t> cls4;
+  if (cls) {
+    cls4.resize(N);
+    for (int c = 0; c < N; ++c) cls4[c] = cls[c] == 0 ? 0 : (uint8_t)(cls[c] + 1);
+    for (int f = 0; f < F; ++f) {
+      const int l = mv.face_left[f];
+      const int r = mv.face_right[f] >= 0 ? mv.face_right[f]
+                    : mv.face_partner[f] >= 0 ? mv.face_left[mv.face_partner[f]] : -1;
+      if (r < 0) continue;
+      if (cls[l] == 0 && cls[r] != 0) cls4[l] = 1;
+      if (cls[r] == 0 && cls[l] != 0) cls4[r] = 1;
+    }
+  }
   std::vector<std::pair<std::pair<int, uint64_t>, int>> key(N);
   for (int c = 0; c < N; ++c) {
     uint64_t k = 0;
@@ -445,14 +479,15 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
       const uint64_t q = (uint64_t)std::min(2097151.0, std::max(0.0, u * 2097151.0));
       k |= spread3(q) << d;
     }
-    key[c] = {{cls ? (int)cls[c] : 0, k}, c};
+    key[c] = {{cls ? (int)cls4[c] : 0, k}, c};
   }
   std::sort(key.begin(), key.end());
-  h.n_own = h.n_k1 = 0;
+  h.n_deep = h.n_own = h.n_k1 = 0;
   for (int c = 0; c < N; ++c) {
-    const int k = cls ? cls[c] : 0;
-    if (k == 0) ++h.n_own;
-    if (k <= 1) ++h.n_k1;
+    const int k = cls ? cls4[c] : 0;
+    if (k == 0) ++h.n_deep;
+    if (k <= 1) ++h.n_own;
+    if (k <= 2) ++h.n_k1;
   }
   h.cperm.resize(N);
   std::vector<int> cinv(N);
@@ -646,10 +681,13 @@ void alloc_state(tafv_gpu& h) {
   h.face_counts = dalloc<int>((size_t)std::max(1, h.ntile_f) * kMaxLevels);
   h.clist = dalloc<int>(N);
   h.flist = dalloc<int>(F);
-  if (h.n_k1 != h.n_own) {
-    h.klist = dalloc<int>(N);
-    h.ntile_k = (int)((h.n_k1 + kTile - 1) / kTile);
+  if (h.n_k1 != h.n_own || h.n_deep != h.n_own) {
+    h.klist = dalloc<int>(std::max(1, h.n_deep));
+    h.ntile_k = (int)((h.n_deep + kTile - 1) / kTile);
     h.k1_counts = dalloc<int>((size_t)std::max(1, h.ntile_k) * kMaxLevels);
+    h.kblist = dalloc<int>(std::max(1, h.n_k1 - h.n_deep));
+    h.ntile_kb = (int)((h.n_k1 - h.n_deep + kTile - 1) / kTile);
+    h.kb_counts = dalloc<int>((size_t)std::max(1, h.ntile_kb) * kMaxLevels);
   } else {
     h.klist = h.clist;
   }
@@ -755,16 +793,27 @@ void collect_times(tafv_gpu& h) {
 
 // ---- halo exchange (shards) -------------------------------------------------
 // Owned rows listed for the peers -> sendbuf -> comm -> recvbuf -> halo rows.
-void halo_rows(tafv_gpu& h, double* arr, int width) {
+// The pack runs on the compute stream right behind the K3 that wrote the
+// rows; the exchange and the unpack run on the comm stream, so the next
+// phase's K1 over the deep cells (which read no halo row) overlaps them.
+// join_now: the compute stream waits for the halo at once (trailing
+// corrector: the plan follows); otherwise the next K1 joins it before its
+// border cells (halo_join).
+void halo_rows(tafv_gpu& h, double* arr, int width, bool join_now) {
   if (!h.sharded()) return;
   if (h.send_total)
     k_pack_rows<<<h.grid_for((long long)h.send_total * width, 256), 256, 0, h.st>>>(
         arr, h.d_send_idx, h.send_total, width, h.sendbuf);
-  h.comm->exchange(h, width * (int)sizeof(double));
+  CK(cudaEventRecord(h.ev_pack, h.st));
+  CK(cudaStreamWaitEvent(h.cst, h.ev_pack, 0));
+  h.comm->exchange(h, width * (int)sizeof(double), h.cst);
   if (h.recv_total)
-    k_unpack_rows<<<h.grid_for((long long)h.recv_total * width, 256), 256, 0, h.st>>>(
+    k_unpack_rows<<<h.grid_for((long long)h.recv_total * width, 256), 256, 0, h.cst>>>(
         h.recvbuf, h.d_recv_idx, h.recv_total, width, arr);
+  CK(cudaEventRecord(h.ev_halo, h.cst));
   h.launches += 2;
+  h.halo_pending = true;
+  if (join_now) halo_join(h);
 }
 
 void halo_i8(tafv_gpu& h, int8_t* arr) {
@@ -773,7 +822,7 @@ void halo_i8(tafv_gpu& h, int8_t* arr) {
   int8_t* rb = reinterpret_cast<int8_t*>(h.recvbuf);
   if (h.send_total)
     k_pack_i8<<<h.grid_for(h.send_total, 256), 256, 0, h.st>>>(arr, h.d_send_idx, h.send_total, sb);
-  h.comm->exchange(h, 1);
+  h.comm->exchange(h, 1, h.st);
   if (h.recv_total)
     k_unpack_i8<<<h.grid_for(h.recv_total, 256), 256, 0, h.st>>>(rb, h.d_recv_idx, h.recv_total, arr);
   h.launches += 2;
@@ -814,10 +863,12 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
     k_tile_count<<<ntc, kCompactThreads, 0, h.st>>>(h.tau, h.n_own, nkeys, h.cell_counts);
     ++h.launches;
   }
-  const bool k1 = h.klist != h.clist;  // shards: K1 list over owned + ring 1
+  const bool k1 = h.klist != h.clist;  // shards: deep and border K1 lists
   if (k1) {
-    k_tile_count<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_k1, nkeys, h.k1_counts);
-    ++h.launches;
+    k_tile_count<<<std::max(1, h.ntile_k), kCompactThreads, 0, h.st>>>(h.tau, h.n_deep, nkeys, h.k1_counts);
+    k_tile_count<<<std::max(1, h.ntile_kb), kCompactThreads, 0, h.st>>>(h.tau + h.n_deep, h.n_k1 - h.n_deep,
+                                                                        nkeys, h.kb_counts);
+    h.launches += 2;
   }
   k_face_cadence<<<std::max(1, (h.F + kTile - 1) / kTile), kCompactThreads, 0, h.st>>>(
       md, h.tau, h.cad, reinterpret_cast<unsigned*>(h.fflag), h.dplan, h.n_own, h.F_own, nkeys, h.face_counts,
@@ -826,14 +877,16 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   // shards' K1 list: prefixes of each are the active sets of every level
   CompactJobs jobs{};
   jobs.j[0] = CompactJob{h.tau, h.n_own, ntc, h.cell_counts, h.clist, &h.dplan->cell_count[0],
-                         &h.dplan->ncell_prefix[0]};
+                         &h.dplan->ncell_prefix[0], 0};
   jobs.j[1] = CompactJob{h.cad, h.F_own, h.ntile_f, h.face_counts, h.flist, &h.dplan->face_count[0],
-                         &h.dplan->nface_prefix[0]};
+                         &h.dplan->nface_prefix[0], 0};
   jobs.njobs = 2;
   if (k1) {
-    jobs.j[2] = CompactJob{h.tau, h.n_k1, std::max(1, h.ntile_k), h.k1_counts, h.klist,
-                           &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0]};
-    jobs.njobs = 3;
+    jobs.j[2] = CompactJob{h.tau, h.n_deep, std::max(1, h.ntile_k), h.k1_counts, h.klist,
+                           &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0], 0};
+    jobs.j[3] = CompactJob{h.tau + h.n_deep, h.n_k1 - h.n_deep, std::max(1, h.ntile_kb), h.kb_counts,
+                           h.kblist, &h.dplan->kb_count[0], &h.dplan->nkb_prefix[0], h.n_deep};
+    jobs.njobs = 4;
   }
   int tiles = 0;
   for (int q = 0; q < jobs.njobs; ++q) tiles += jobs.j[q].ntiles;
@@ -1068,7 +1121,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     na += h.ccount[l];
     nf += h.fcount[l];
   }
-  nk = h.klist == h.clist ? na : h.n_k1;  // shards: K1 over owned + ring 1 (upper bound)
+  nk = h.klist == h.clist ? na : h.n_deep;  // shards: deep cells (upper bound); border below
   // Level theta activates every cell and face (tau <= theta): identity lists
   // (owned / owned + ring 1 / faces touching owned lead the internal order).
   const bool all = level == h.theta;
@@ -1077,6 +1130,8 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const int* fl = all ? nullptr : h.flist;
   const int* ncp = &h.dplan->ncell_prefix[level];
   const int* nkp = &h.dplan->nk1_prefix[level];
+  const int* nkbp = &h.dplan->nkb_prefix[level];
+  const int* kbl = all ? nullptr : h.kblist;
   const int* nfp = &h.dplan->nface_prefix[level];
   const MeshDev md = h.mesh_dev();
   const StateDev sd = h.state_dev();
@@ -1089,8 +1144,17 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
   timed(h, tafv_gpu::kK1, [&] {
-    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, front, pred ? 1 : 0, h.next_dir());
+    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
   }, na, nf, nfr);
+  if (h.sharded()) {
+    // border cells (owned next to the halo, ring 1) once the halo landed
+    halo_join(h);
+    const int gb = fixed ? h.grid_k1 : h.grid_for(h.n_k1 - h.n_deep, 128);
+    timed(h, tafv_gpu::kK1, [&] {
+      k_grad_limit<P, DEG><<<gb, 128, 0, h.st>>>(md, sd, kbl, nkbp, h.n_deep, front, pred ? 1 : 0, 0);
+    }, 0, 0, 0);
+    ++h.launches;
+  }
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     const int r2 = h.next_dir();
     if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan, r2);
@@ -1107,7 +1171,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
       h.comm->allreduce_sum_f64(h.rank, h.dplan->totals, P::NV, h.st);
       h.comm->allreduce_max_i32(h.rank, &h.dplan->nonfinite, 1, h.st);
     }
-    halo_rows(h, h.w, P::NV);  // the next iteration stages the halo's new w
+    halo_rows(h, h.w, P::NV, true);  // the next iteration stages the halo's new w
   } else {
     timed(h, pred ? tafv_gpu::kK3P : tafv_gpu::kK3C, [&] {
       const int r3 = h.next_dir();
@@ -1119,7 +1183,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     h.launches += 3;
     // shards: the just-updated rows of owned cells to the peers' halos
     // (w_pred after a predictor, w after a corrector)
-    halo_rows(h, pred ? h.wp : h.w, P::NV);
+    halo_rows(h, pred ? h.wp : h.w, P::NV, false);
   }
 }
 
@@ -1176,7 +1240,9 @@ void run_sweep(tafv_gpu& h) {
     h.capturing = false;
     h.cap = nullptr;
     CK(e);
-    CK(cudaGraphInstantiate(&rec.exec, g, 0));
+    // node priorities: the halo exchange captured from the high-priority
+    // comm stream keeps its priority over the K1 it overlaps
+    CK(cudaGraphInstantiate(&rec.exec, g, cudaGraphInstantiateFlagUseNodePriority));
     CK(cudaGraphDestroy(g));
     rec.launches = h.launches - l0;
     h.launches = l0;
@@ -1326,6 +1392,13 @@ static int create_handle(const tafv_mesh_view* mesh, const tafv_physics* physics
   try {
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&h->cst, cudaStreamNonBlocking, hi));
+      CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+    }
     CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
     h->grid_cap = h->sms * 16;
     h->model = physics->model;
