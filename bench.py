@@ -277,7 +277,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--flag", action="append", default=[],
                     help="library launch knob name=value (tafv_gpu_set_flag), for A/B runs")
     args = ap.parse_args()

@@ -921,6 +921,15 @@ __global__ void k_select_sweep(const PlanDev* plan, cudaGraphConditionalHandle h
 }
 
 // Halo rows: pack owned rows for the peers, unpack received halo rows.
+// The device plan into pinned host memory (mapped, written over the link by
+// the SMs: no copy engine).
+__global__ void k_store_plan(const PlanDev* __restrict__ src, PlanDev* dst) {
+  static_assert(sizeof(PlanDev) % 8 == 0, "PlanDev is copied in 8-byte words");
+  const unsigned long long* a = reinterpret_cast<const unsigned long long*>(src);
+  unsigned long long* b = reinterpret_cast<unsigned long long*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(PlanDev) / 8); i += blockDim.x) b[i] = a[i];
+}
+
 __global__ void k_pack_rows(const double* src, const int* idx, int n, int width, double* dst) {
   const size_t total = (size_t)n * width;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -949,6 +958,21 @@ __global__ void k_gather_rows(const double* src, const int* perm, int n, int wid
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
     const size_t row = i / width, col = i % width;
     dst[i] = src[(size_t)perm[row] * width + col];
+  }
+}
+
+// A state given as W alone, in original row order: W gathered into the
+// internal order and w = W / V (intensive_correct, kernels.cpp:237-241), one
+// pass (k_gather_rows + k_intensive fused).
+__global__ void k_load_extensive(const double* src, const int* perm, const double* vol, int n, int width,
+                                 double* W, double* w) {
+  const size_t total = (size_t)n * width;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const size_t row = i / width, col = i % width;
+    const double v = src[(size_t)perm[row] * width + col];
+    W[i] = v;
+    w[i] = v / vol[row];
   }
 }
 

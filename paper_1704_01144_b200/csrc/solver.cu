@@ -137,6 +137,7 @@ struct tafv_gpu {
   double4* sgeo = nullptr;  // hex fast path per-slot geometry (see MeshDev)
   double4* sdx = nullptr;
   bool slot_geo = true;
+  int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
@@ -298,6 +299,15 @@ void halo_join(tafv_gpu& h) {
   if (!h.halo_pending) return;
   CK(cudaStreamWaitEvent(h.st, h.ev_halo, 0));
   h.halo_pending = false;
+}
+
+// The device plan into the pinned host copy by a one-block kernel (stores
+// over the link into mapped memory): a copy-engine transfer here would queue
+// behind any bulk device-to-host copy in flight (run_batch's downloads, a
+// caller's copies) and stall the library stream for its duration.
+void store_plan(tafv_gpu& h) {
+  k_store_plan<<<1, 128, 0, h.st>>>(h.dplan, h.hplan);
+  ++h.launches;
 }
 
 // ---- transports (comm.h) ------------------------------------------------------
@@ -895,7 +905,7 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   h.launches += 3;
   if (h.sharded()) h.comm->allreduce_sum_i64(h.rank, &h.dplan->gcell_count[0], kMaxLevels, h.st);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+  store_plan(h);
   h.plan_nkeys = nkeys;
 }
 
@@ -1283,7 +1293,7 @@ void run_iteration(tafv_gpu& h, tafv_record* rec) {
   CK(cudaEventRecord(h.ev[0], h.st));
   run_sweep(h);
   CK(cudaEventRecord(h.ev[1], h.st));
-  CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+  store_plan(h);
   CK(cudaStreamSynchronize(h.st));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
@@ -1315,7 +1325,7 @@ void integrate_pipelined(tafv_gpu& h, const tafv_options& opt, int n, tafv_recor
     if (more) {
       enqueue_plan(h, opt);
     } else {
-      CK(cudaMemcpyAsync(h.hplan, h.dplan, sizeof(PlanDev), cudaMemcpyDeviceToHost, h.st));
+      store_plan(h);
     }
     CK(cudaStreamSynchronize(h.st));
     collect_times(h);
@@ -1804,8 +1814,7 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
       if (j + 1 < n_inputs) upload(j + 1);
       // state j: W from the staged input, w = W / V (kernels.cpp:237-241)
       CK(cudaStreamWaitEvent(h->st, h->ev_in[q], 0));
-      k_gather_rows<<<grid, 256, 0, h->st>>>(h->bin[q], h->d_cperm, h->N, h->nv, h->W);
-      k_intensive<<<grid, 256, 0, h->st>>>(h->W, h->vol, h->N, h->nv, h->w);
+      k_load_extensive<<<grid, 256, 0, h->st>>>(h->bin[q], h->d_cperm, h->vol, h->N, h->nv, h->W, h->w);
       CK(cudaEventRecord(h->ev_in_free[q], h->st));
       h->t0 = 0.0;
       h->iteration = 0;
@@ -1815,19 +1824,29 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
         for (int it = 0; it < iterations; ++it) {
           CK(cudaGraphLaunch(h->iter_graph, h->st));
           // this iteration's plan + its sweep's flags and totals
-          CK(cudaMemcpyAsync(&h->batch_plans[(size_t)j * iterations + it], h->dplan, sizeof(PlanDev),
-                             cudaMemcpyDeviceToHost, h->st));
+          // stored by a kernel into the pinned (device-mapped) host array:
+          // a copy-engine transfer would queue behind the bulk download of
+          // the previous input on the same engine and stall this stream
+          k_store_plan<<<1, 128, 0, h->st>>>(h->dplan, &h->batch_plans[(size_t)j * iterations + it]);
         }
       } else {
         integrate_pipelined(*h, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
       }
-      // output j: W in original order -> staging -> host. On the library
-      // stream: a device-to-host copy running under the kernels was measured
-      // to slow them ~2x, so only the uploads overlap compute.
+      // output j: W in original order -> staging -> host on the download
+      // copy stream, under input j+1's compute. (A copy-engine read-back of
+      // the plan on the library stream queued behind these downloads and
+      // stalled it; the plan now goes to the host by a kernel, store_plan.)
       CK(cudaStreamWaitEvent(h->st, h->ev_out_free[q], 0));
       k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[q]);
-      CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->st));
-      CK(cudaEventRecord(h->ev_out_free[q], h->st));
+      if (h->dl_stream) {
+        CK(cudaEventRecord(h->ev_out[q], h->st));
+        CK(cudaStreamWaitEvent(h->cout, h->ev_out[q], 0));
+        CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->cout));
+        CK(cudaEventRecord(h->ev_out_free[q], h->cout));
+      } else {
+        CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaEventRecord(h->ev_out_free[q], h->st));
+      }
     }
     CK(cudaStreamSynchronize(h->cout));
     CK(cudaStreamSynchronize(h->cin));
@@ -1923,6 +1942,8 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
         for (auto e : g.second.evs) cudaEventDestroy(e);
       }
       h->graphs.clear();
+    } else if (n == "dl_stream") {
+      h->dl_stream = (int)value;
     } else if (n == "plan_graph") {
       h->plan_graph_on = value != 0;
     } else if (n == "use_graph") {
