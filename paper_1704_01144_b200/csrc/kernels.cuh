@@ -175,6 +175,9 @@ __device__ __forceinline__ void st2(double* p, double a, double b) {
 __device__ __forceinline__ int slot_face(int e) { return e >= 0 ? e : ~e; }
 __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0; }
 
+#ifndef TAFV_BJ2
+#define TAFV_BJ2 1
+#endif
 // Barth-Jespersen update alpha = min(alpha, minmod(delta, head) / delta)
 // (kernels.cpp:111-117) with the division evaluated only where its value can
 // matter. Exactly equivalent, including signed zeros and NaN:
@@ -183,7 +186,24 @@ __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0;
 //   opposite sign / zero / NaN head -> 0.0/delta = +-0 by the sign of delta;
 //   delta NaN                      -> NaN ratio: smin leaves alpha unchanged;
 //   delta == 0                     -> skipped by the reference.
-__device__ __forceinline__ double bj_update(double alpha, double delta, double head) {
+__device__ __forceinline__ double bj_update(double alpha, double delta, double hp, double hn) {
+#if TAFV_BJ2
+  // In magnitudes: A = the headroom on delta's side, sign-normalised (hp =
+  // w_max - w_c for delta > 0, hn = -(w_min - w_c) for delta < 0, exact).
+  //   A > 0, |delta| > A      -> head / delta = A / |delta| (IEEE division is
+  //                              sign-symmetric: the same quotient)
+  //   A > 0, |delta| <= A     -> 1 (or NaN for inf/inf): no-op
+  //   A <= 0 or NaN           -> +-0 by the sign of delta
+  //   delta == 0 or NaN       -> skipped / no-op
+  const bool pos = delta > 0.0, neg = delta < 0.0;
+  const double A = pos ? hp : hn;
+  const bool aok = A > 0.0;
+  const double ad = fabs(delta);
+  if ((pos || neg) && !aok) alpha = smin(alpha, pos ? 0.0 : -0.0);
+  if (aok && ad > A) alpha = smin(alpha, A / ad);
+  return alpha;
+#else
+  const double head = delta > 0.0 ? hp : -hn;
   // zero outcome (opposite signs, head == 0 or NaN): +0 for delta > 0, -0 for
   // delta < 0 -- predicated; the quotient only where |head| < |delta|.
   const bool pos = delta > 0.0, neg = delta < 0.0;
@@ -192,6 +212,7 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
   if ((pos || neg) && !same) alpha = smin(alpha, pos ? 0.0 : -0.0);
   if (lim) alpha = smin(alpha, head / delta);
   return alpha;
+#endif
 }
 
 // ---- K1: stage + Green-Gauss + Barth-Jespersen ----------------------------
@@ -286,8 +307,8 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #pragma unroll
       for (int k = 0; k < NV; ++k) {
         alpha[k] = 1.0;
-        wmax[k] = wmax[k] - we[k];
-        wmin[k] = wmin[k] - we[k];
+        wmax[k] = wmax[k] - we[k];     // hp: headroom above
+        wmin[k] = -(wmin[k] - we[k]);  // hn: headroom below, negated (exact)
       }
 #pragma unroll
       for (int t = s0; t < s1; ++t) {
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
         for (int k = 0; k < NV; ++k) {
           double delta = g[k][0] * dx0 + g[k][1] * dx1;
           if (D == 3) delta = delta + g[k][D - 1] * dx2;
-          alpha[k] = bj_update(alpha[k], delta, delta > 0.0 ? wmax[k] : wmin[k]);
+          alpha[k] = bj_update(alpha[k], delta, wmax[k], wmin[k]);
         }
       }
 #pragma unroll
