@@ -58,6 +58,11 @@ struct MeshDev {
   // kernel would compute: sign*area is exact, the subtraction is the same).
   const double4* __restrict__ sgeo;  // [N*6]
   const double4* __restrict__ sdx;   // [N*6] {dx, dy, dz, 0}: one 256-bit load per slot
+  // [2F] or null: K2's reconstruction offsets per face, fc - c_left and
+  // fc' - c_right (fc' = the partner's centroid across a periodic link), as
+  // {dLx, dLy, dLz, 0}, {dRx, dRy, dRz, 0}: the same IEEE differences the
+  // kernel would form, loaded by face index instead of gathered by cell.
+  const double4* __restrict__ fdx;
 };
 
 struct StateDev {
@@ -353,7 +358,13 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
   }
 }
 
-// kernels.cpp:25-27 with the z term appended left to right.
+// kernels.cpp:25-27 with the z term appended left to right; d = to - from.
+template <int D>
+__device__ __forceinline__ double extrapolate_d(double w, const double* g, const double* d) {
+  double v = (w + g[0] * d[0]) + g[1] * d[1];
+  if (D == 3) v = v + g[D - 1] * d[D - 1];
+  return v;
+}
 template <int D>
 __device__ __forceinline__ double extrapolate(double w, const double* g, const double* from,
                                               const double* to) {
@@ -396,7 +407,6 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     const int2 lr = m.lr[f];
     const double4 gm = ld4(m.geo + f);
     const double nrm[3] = {gm.x, gm.y, gm.z};
-    const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
     double wL[NV], wR[NV];
     int tl;
     {
@@ -404,9 +414,17 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
       tl = stage_spec<NV>(s, lr.x, front, PRED, we);
       double g[GradRow<NV>::S];
       load_grad<NV>(s, lr.x, g);
-      const double cl[3] = {m.cen[3 * (size_t)lr.x], m.cen[3 * (size_t)lr.x + 1], m.cen[3 * (size_t)lr.x + 2]};
+      if (m.fdx) {
+        const double4 a = ld4(m.fdx + 2 * (size_t)f);
+        const double dl[3] = {a.x, a.y, a.z};
 #pragma unroll
-      for (int k = 0; k < NV; ++k) wL[k] = extrapolate<D>(we[k], g + 3 * k, cl, fc);
+        for (int k = 0; k < NV; ++k) wL[k] = extrapolate_d<D>(we[k], g + 3 * k, dl);
+      } else {
+        const double fc[3] = {m.fcen[3 * (size_t)f], m.fcen[3 * (size_t)f + 1], m.fcen[3 * (size_t)f + 2]};
+        const double cl[3] = {m.cen[3 * (size_t)lr.x], m.cen[3 * (size_t)lr.x + 1], m.cen[3 * (size_t)lr.x + 2]};
+#pragma unroll
+        for (int k = 0; k < NV; ++k) wL[k] = extrapolate<D>(we[k], g + 3 * k, cl, fc);
+      }
       if (!P::admissible(pp, wL)) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) wL[k] = we[k];
@@ -421,11 +439,18 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
       double g[GradRow<NV>::S];
       load_grad<NV>(s, lr.y, g);
-      const double cr[3] = {m.cen[3 * (size_t)lr.y], m.cen[3 * (size_t)lr.y + 1], m.cen[3 * (size_t)lr.y + 2]};
-      const double* to = m.fcen + 3 * (size_t)(m.rcf ? m.rcf[f] : f);
-      const double tc[3] = {to[0], to[1], to[2]};
+      if (m.fdx) {
+        const double4 b = ld4(m.fdx + 2 * (size_t)f + 1);
+        const double dr[3] = {b.x, b.y, b.z};
 #pragma unroll
-      for (int k = 0; k < NV; ++k) wR[k] = extrapolate<D>(we[k], g + 3 * k, cr, tc);
+        for (int k = 0; k < NV; ++k) wR[k] = extrapolate_d<D>(we[k], g + 3 * k, dr);
+      } else {
+        const double cr[3] = {m.cen[3 * (size_t)lr.y], m.cen[3 * (size_t)lr.y + 1], m.cen[3 * (size_t)lr.y + 2]};
+        const double* to = m.fcen + 3 * (size_t)(m.rcf ? m.rcf[f] : f);
+        const double tc[3] = {to[0], to[1], to[2]};
+#pragma unroll
+        for (int k = 0; k < NV; ++k) wR[k] = extrapolate<D>(we[k], g + 3 * k, cr, tc);
+      }
       if (!P::admissible(pp, wR)) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) wR[k] = we[k];

@@ -136,7 +136,9 @@ struct tafv_gpu {
   double4* geo = nullptr;
   double4* sgeo = nullptr;  // hex fast path per-slot geometry (see MeshDev)
   double4* sdx = nullptr;
+  double4* fdx = nullptr;  // see MeshDev::fdx
   bool slot_geo = true;
+  bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
@@ -236,7 +238,7 @@ struct tafv_gpu {
   MeshDev mesh_dev() const {
     return MeshDev{N,    F,   vol,    ivol,   cen,  chl, adj_off, adj_face, adj_nb, lr,
                    periodic ? rcf : nullptr, geo, fcen, slot_geo ? sgeo : nullptr,
-                   slot_geo ? sdx : nullptr};
+                   slot_geo ? sdx : nullptr, face_dx ? fdx : nullptr};
   }
   StateDev state_dev() const {
     return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr};
@@ -266,7 +268,7 @@ struct tafv_gpu {
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
     if (batch_plans) cudaFreeHost(batch_plans);
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
-    void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,      adj_off, adj_face,
+    void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,   fdx,   adj_off, adj_face,
                     adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
@@ -624,6 +626,25 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
     up(h.sgeo, sgeo);
     h.sdx = dalloc<double4>(h.M);
     up(h.sdx, sdx);
+  }
+  {
+    // K2 reconstruction offsets per face (MeshDev::fdx), the kernel's own
+    // differences: face centroid minus left centroid, (partner) face centroid
+    // minus right centroid
+    std::vector<double4> fdx(2 * (size_t)F, make_double4(0.0, 0.0, 0.0, 0.0));
+    for (int j = 0; j < F; ++j) {
+      const int l = lr[j].x, r = lr[j].y;
+      double dl[3], dr[3] = {0.0, 0.0, 0.0};
+      for (int d = 0; d < 3; ++d) dl[d] = fcen[3 * (size_t)j + d] - cen[3 * (size_t)l + d];
+      if (r >= 0) {
+        const int t = h.periodic ? rcf[j] : j;
+        for (int d = 0; d < 3; ++d) dr[d] = fcen[3 * (size_t)t + d] - cen[3 * (size_t)r + d];
+      }
+      fdx[2 * (size_t)j] = make_double4(dl[0], dl[1], dl[2], 0.0);
+      fdx[2 * (size_t)j + 1] = make_double4(dr[0], dr[1], dr[2], 0.0);
+    }
+    h.fdx = dalloc<double4>(2 * (size_t)F);
+    up(h.fdx, fdx);
   }
   h.cen = dalloc<double>(3 * (size_t)N);
   up(h.cen, cen);
@@ -1944,6 +1965,13 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
       h->graphs.clear();
     } else if (n == "dl_stream") {
       h->dl_stream = (int)value;
+    } else if (n == "face_dx") {
+      h->face_dx = value != 0;
+      for (auto& g : h->graphs) {
+        cudaGraphExecDestroy(g.second.exec);
+        for (auto e : g.second.evs) cudaEventDestroy(e);
+      }
+      h->graphs.clear();
     } else if (n == "plan_graph") {
       h->plan_graph_on = value != 0;
     } else if (n == "use_graph") {
