@@ -188,6 +188,7 @@ struct tafv_gpu {
   // hot launch, summed per kind after the call's host sync.
   enum { kK1 = 0, kK2P, kK2C, kK3P, kK3C, kPlan, kNumKinds };
   bool ktime = false;
+  bool klog = getenv("TAFV_KLOG") != nullptr;  // per-launch times on stderr (kernel_timing runs)
   std::vector<cudaEvent_t> evpool;
   std::vector<int> evkind;
   double kms[kNumKinds] = {};
@@ -807,6 +808,11 @@ void collect_times(tafv_gpu& h) {
     for (size_t i = 0; i < g.kinds.size(); ++i) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, g.evs[2 * i], g.evs[2 * i + 1]));
+      // per-launch log (kind, active cells / faces / fringe at capture, us):
+      // tools/klog_summary.py, tools/small_phase_probe.py
+      if (h.klog)
+        fprintf(stderr, "KLOG %d %lld %lld %lld %.4f\n", g.kinds[i], g.items[i][0], g.items[i][1], g.items[i][2],
+                ms * 1e3);
       h.kms[g.kinds[i]] += ms;
       h.kcnt[g.kinds[i]] += 1;
       for (int j = 0; j < 3; ++j) h.kitems[g.kinds[i]][j] += g.items[i][j];
