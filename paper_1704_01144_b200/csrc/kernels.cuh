@@ -392,11 +392,12 @@ __device__ __forceinline__ void load_grad(const StateDev& s, int x, double* g) {
 #ifndef TAFV_K2_MINB
 #define TAFV_K2_MINB 7
 #endif
-template <class P, bool PRED>
+template <class P, bool PRED, bool SEL = false>
 __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
                                                    const int* __restrict__ list,
                                                    const int* __restrict__ n_dev, int front,
-                                                   const PlanDev* __restrict__ plan, int rev) {
+                                                   const PlanDev* __restrict__ plan, int rev,
+                                                   const uint8_t* __restrict__ sel, int selv) {
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
   const double dt = plan->dt_min;
@@ -404,6 +405,10 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
   for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
     const int i = rev ? n - 1 - ii : ii;
     const int f = list ? list[i] : i;
+    // shards: the pass over the interior faces (both sides deep owned: their
+    // gradients come from the K1 over the deep cells) runs while the halo
+    // is in flight; the other faces after the join (sel = face class)
+    if (SEL && sel[f] != selv) continue;
     const int2 lr = m.lr[f];
     const double4 gm = ld4(m.geo + f);
     const double nrm[3] = {gm.x, gm.y, gm.z};

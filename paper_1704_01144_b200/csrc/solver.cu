@@ -209,6 +209,7 @@ struct tafv_gpu {
   int *d_send_idx = nullptr, *d_recv_idx = nullptr;
   int send_total = 0, recv_total = 0;
   double *sendbuf = nullptr, *recvbuf = nullptr;
+  uint8_t* fint = nullptr;    // shards: [F] 1 = face whose sides are deep owned cells (or boundary of one)
   int* klist = nullptr;       // K1 list of the deep cells; == clist when single domain
   int* kblist = nullptr;      // K1 list of the border cells (owned next to the halo + ring 1)
   int* k1_counts = nullptr;
@@ -274,7 +275,7 @@ struct tafv_gpu {
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
-                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts};
+                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, fint};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
@@ -598,6 +599,13 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
     for (int d = 0; d < 3; ++d) fcen[3 * (size_t)j + d] = mv.face_centroid[3 * (size_t)f + d];
   }
   h.vol_host = vol;
+  if (cls) {
+    std::vector<uint8_t> fint(F);
+    for (int j = 0; j < F; ++j)
+      fint[j] = lr[j].x < h.n_deep && (lr[j].y < 0 || lr[j].y < h.n_deep) ? 1 : 0;
+    h.fint = dalloc<uint8_t>(std::max(1, F));
+    CK(cudaMemcpy(h.fint, fint.data(), F, cudaMemcpyHostToDevice));
+  }
 
   auto up = [&](auto* dst, const auto& src) {
     CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(src[0]), cudaMemcpyHostToDevice));
@@ -1183,7 +1191,14 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   timed(h, tafv_gpu::kK1, [&] {
     k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
   }, na, nf, nfr);
+  const PlanDev* cpl = h.dplan;
   if (h.sharded()) {
+    // interior faces while the halo is in flight
+    timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
+      if (pred) k_face_flux<P, true, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, 0, h.fint, 1);
+      else k_face_flux<P, false, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, 0, h.fint, 1);
+    }, 0, 0, 0);
+    ++h.launches;
     // border cells (owned next to the halo, ring 1) once the halo landed
     halo_join(h);
     const int gb = fixed ? h.grid_k1 : h.grid_for(h.n_k1 - h.n_deep, 128);
@@ -1194,8 +1209,13 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   }
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     const int r2 = h.next_dir();
-    if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan, r2);
-    else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, h.dplan, r2);
+    if (h.sharded()) {  // the faces left after the interior pass
+      if (pred) k_face_flux<P, true, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, h.fint, 0);
+      else k_face_flux<P, false, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, h.fint, 0);
+    } else {
+      if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, nullptr, 0);
+      else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, nullptr, 0);
+    }
   }, na, nf, nfr);
   if (last) {
     timed(h, tafv_gpu::kK3C, [&] {
