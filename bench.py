@@ -348,9 +348,9 @@ def main():
     value = ceff / (ms / 1e3)
 
     # per-kernel breakdown: replay the SAME K iterations (state restored,
-    # deterministic => identical plans) with CUDA events around every kernel
-    # on the library stream (direct launches; events cannot sit inside the
-    # replayed graph without perturbing it).
+    # deterministic => identical plans) with event-record nodes around every
+    # hot kernel inside the same captured sweep graphs (the records add a few
+    # microseconds per kernel: shares, not absolutes, are what this explains).
     s.set_state(w_start, W_start, t_start, it_start)
     s.set_flag("kernel_timing", 1)
     recs_k = s.reference_integrate(opt, args.steps)
