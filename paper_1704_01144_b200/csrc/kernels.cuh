@@ -651,16 +651,19 @@ __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParam
     const double b = tau_scale ? d / (double)(1 << tau_scale[c]) : d;
     lowest = smin(lowest, b);
   }
-  __shared__ double red[256];
+  // warp-shuffle then per-warp minima (dt_max is never NaN: a NaN speed
+  // takes dt_cap, so the order of the exact minimum does not matter)
+  __shared__ double red[8];
   __shared__ bool last;
   auto block_reduce = [&](double v) {
-    red[threadIdx.x] = v;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = smin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] = smin(red[threadIdx.x], red[threadIdx.x + w]);
-      __syncthreads();
-    }
-    return red[0];
+    double r = red[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) r = smin(r, red[q]);
+    __syncthreads();
+    return r;
   };
   const double bm = block_reduce(lowest);
   if (threadIdx.x == 0) {

@@ -713,7 +713,10 @@ void alloc_state(tafv_gpu& h) {
   CK(cudaMemset(h.tau, 0, N));
   CK(cudaMemset(h.cad, 0, F));
   h.dtmax = dalloc<double>(N);
-  h.nblk_dt = h.sms * 4;
+#ifndef TAFV_DT_BPS
+#define TAFV_DT_BPS 4
+#endif
+  h.nblk_dt = h.sms * TAFV_DT_BPS;
   h.blockmin = dalloc<double>(h.nblk_dt);
   h.ntile_c = (int)((h.n_own + kTile - 1) / kTile);
   h.ntile_f = (int)((h.F_own + kTile - 1) / kTile);
