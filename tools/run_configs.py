@@ -31,6 +31,9 @@ def load_peak():
         return 6650.0
 
 
+FLAGS = []
+
+
 def run(cfg, iters, tau0=None):
     """One warm-up iteration (graph capture; excluded), then `iters` timed
     iterations as plan_iteration + run_iteration (device time of both from
@@ -42,6 +45,9 @@ def run(cfg, iters, tau0=None):
     w0 = cfg.initial_state(mesh)
     t = time.perf_counter()
     s = Solver(mesh, "euler")
+    for fv in FLAGS:
+        k, v = fv.split("=")
+        s.set_flag(k, int(v))
     t_up = time.perf_counter() - t
     s.set_state(w0)
     opt = cfg.options()
@@ -95,6 +101,7 @@ def main():
     ap.add_argument("configs", nargs="+", type=int)
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--tau0", default="0.01,0.1,0.5")
+    ap.add_argument("--flag", action="append", default=[], help="library knob name=value (A/B)")
     a = ap.parse_args()
     for cid in a.configs:
         cfg = configs.get(cid)
