@@ -140,6 +140,13 @@ struct tafv_gpu {
   bool slot_geo = true;
   bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
+  // run_batch lanes: a twin handle sharing this one's (read-only) mesh arrays
+  // with its own state, plan, graphs and streams, so two independent inputs
+  // advance concurrently and each fills the other's idle SMs (small level
+  // phases, kernel tails). Owned; rebuilt after any set_flag.
+  tafv_gpu* twin = nullptr;
+  bool owns_mesh = true;
+  int batch_lanes = 2;
   int *d_cperm = nullptr, *d_fperm = nullptr;
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
@@ -263,6 +270,7 @@ struct tafv_gpu {
 
   ~tafv_gpu() {
     cudaSetDevice(device);
+    delete twin;
     for (auto& g : graphs) {
       cudaGraphExecDestroy(g.second.exec);
       for (auto e : g.second.evs) cudaEventDestroy(e);
@@ -270,12 +278,17 @@ struct tafv_gpu {
     if (plan_graph) cudaGraphExecDestroy(plan_graph);
     if (batch_plans) cudaFreeHost(batch_plans);
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
-    void* ptrs[] = {vol,  ivol,  cen,      chl,      fcen,   sgeo,   sdx,   fdx,   adj_off, adj_face,
-                    adj_nb, lr,  rcf,      geo,      d_cperm, d_fperm, w,     W,        wp,
+    if (owns_mesh) {
+      void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
+                           d_cperm, d_fperm, fint};
+      for (void* p : mesh_ptrs)
+        if (p) cudaFree(p);
+    }
+    void* ptrs[] = {w,     W,        wp,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
-                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, fint};
+                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
@@ -1814,6 +1827,97 @@ void build_iter_graph(tafv_gpu& h, const tafv_options& opt) {
   h.launches = l0;
 }
 
+// The run_batch twin of a single-domain handle (see tafv_gpu::twin), or
+// null when the device lacks the memory for a second state.
+tafv_gpu* make_twin(const tafv_gpu& h) {
+  const size_t state_bytes = (size_t)h.N * (3 * h.nv + h.gs + 8) * sizeof(double) +
+                             (size_t)h.F * (3 * h.fs + 4) * sizeof(double) +
+                             2 * 2 * (size_t)h.N * h.nv * sizeof(double);
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  if (free_b < state_bytes + state_bytes / 2 + ((size_t)1 << 30)) return nullptr;
+  auto* t = new tafv_gpu;
+  try {
+    t->device = h.device;
+    CK(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking));
+    t->model = h.model;
+    t->nv = h.nv;
+    t->dim = h.dim;
+    t->pp = h.pp;
+    t->N = h.N;
+    t->F = h.F;
+    t->M = h.M;
+    t->periodic = h.periodic;
+    t->sms = h.sms;
+    t->grid_cap = h.grid_cap;
+    t->vol_host = h.vol_host;
+    t->owns_mesh = false;
+    t->vol = h.vol;
+    t->ivol = h.ivol;
+    t->cen = h.cen;
+    t->chl = h.chl;
+    t->fcen = h.fcen;
+    t->deg6 = h.deg6;
+    t->adj_off = h.adj_off;
+    t->adj_face = h.adj_face;
+    t->adj_nb = h.adj_nb;
+    t->lr = h.lr;
+    t->rcf = h.rcf;
+    t->geo = h.geo;
+    t->sgeo = h.sgeo;
+    t->sdx = h.sdx;
+    t->fdx = h.fdx;
+    t->d_cperm = h.d_cperm;
+    t->d_fperm = h.d_fperm;
+    t->slot_geo = h.slot_geo;
+    t->face_dx = h.face_dx;
+    t->iwin_alias = h.iwin_alias;
+    t->alt_dir = h.alt_dir;
+    t->use_graph = h.use_graph;
+    t->plan_graph_on = h.plan_graph_on;
+    t->dl_stream = h.dl_stream;
+    t->n_deep = h.n_deep;
+    t->n_own = h.n_own;
+    t->n_k1 = h.n_k1;
+    t->F_own = h.F_own;
+    t->N_global = h.N_global;
+    alloc_state(*t);
+    set_grids(*t);
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+// Run-batch staging of one lane: copy streams, double-buffered device
+// input / output rows, their events; one-graph iteration and plan copies.
+void batch_setup(tafv_gpu& g, const tafv_options& opt, size_t n_plans, bool one_graph) {
+  const size_t n = (size_t)g.N * g.nv;
+  if (!g.cin) {
+    CK(cudaStreamCreateWithFlags(&g.cin, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g.cout, cudaStreamNonBlocking));
+    for (int q = 0; q < 2; ++q) {
+      g.bin[q] = dalloc<double>(n);
+      g.bout[q] = dalloc<double>(n);
+      for (cudaEvent_t* e : {&g.ev_in[q], &g.ev_in_free[q], &g.ev_out[q], &g.ev_out_free[q]}) {
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CK(cudaEventRecord(*e, g.st));  // initially complete
+      }
+    }
+  }
+  if (one_graph) {
+    const bool same = g.iter_graph && g.iter_opt.theta_max == opt.theta_max && g.iter_opt.cfl == opt.cfl &&
+                      g.iter_opt.dt_cap == opt.dt_cap;
+    if (!same) build_iter_graph(g, opt);
+    if (n_plans > g.batch_cap) {
+      if (g.batch_plans) CK(cudaFreeHost(g.batch_plans));
+      CK(cudaMallocHost(&g.batch_plans, n_plans * sizeof(PlanDev)));
+      g.batch_cap = n_plans;
+    }
+  }
+}
+
 // A batch of independent inputs through one handle, each `iterations`
 // iterations from its own extensive state (w = W / V); input j+1 uploads on
 // a copy stream while input j computes on the library stream.
@@ -1823,103 +1927,108 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
     require(opt != nullptr && W_in != nullptr && W_out != nullptr, "run_batch: null argument");
     require(n_inputs >= 0 && iterations >= 1, "run_batch: counts");
     const size_t n = (size_t)h->N * h->nv, bytes = n * sizeof(double);
-    if (!h->cin) {
-      CK(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking));
-      for (int q = 0; q < 2; ++q) {
-        h->bin[q] = dalloc<double>(n);
-        h->bout[q] = dalloc<double>(n);
-        for (cudaEvent_t* e : {&h->ev_in[q], &h->ev_in_free[q], &h->ev_out[q], &h->ev_out_free[q]}) {
-          CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-          CK(cudaEventRecord(*e, h->st));  // initially complete
-        }
-      }
+    // single domain: every iteration is one graph launch (plan + switch to
+    // the sweep of its theta), no host synchronisation inside the batch, and
+    // the inputs alternate between two lanes (this handle and its twin) that
+    // run concurrently; the last input runs on this handle, so its state is
+    // the last input's afterwards
+    const bool one_graph = !h->sharded() && h->use_graph && h->plan_graph_on && !h->ktime;
+    std::vector<tafv_gpu*> lanes{h};
+    if (one_graph && n_inputs >= 2 && h->batch_lanes >= 2) {
+      if (!h->twin) h->twin = make_twin(*h);
+      if (h->twin) lanes.push_back(h->twin);
     }
-    auto upload = [&](int j) {
-      const int q = j & 1;
-      CK(cudaStreamWaitEvent(h->cin, h->ev_in_free[q], 0));
+    const int nl = (int)lanes.size();
+    auto lane_of = [&](int j) { return (n_inputs - 1 - j) % nl; };
+    std::vector<std::vector<int>> mine(nl);  // each lane's inputs, in order
+    for (int j = 0; j < n_inputs; ++j) mine[lane_of(j)].push_back(j);
+    for (int L = 0; L < nl; ++L) batch_setup(*lanes[L], *opt, mine[L].size() * (size_t)iterations, one_graph);
+
+    auto upload = [&](int L, int i) {  // lane-local input i
+      tafv_gpu& g = *lanes[L];
+      const int q = i & 1;
+      CK(cudaStreamWaitEvent(g.cin, g.ev_in_free[q], 0));
       // not under the previous download either (they share the link: measured)
-      CK(cudaStreamWaitEvent(h->cin, h->ev_out_free[q], 0));  // download j - 2 of this slot pair = the one in flight
-      CK(cudaMemcpyAsync(h->bin[q], W_in[j], bytes, cudaMemcpyHostToDevice, h->cin));
-      CK(cudaEventRecord(h->ev_in[q], h->cin));
+      CK(cudaStreamWaitEvent(g.cin, g.ev_out_free[q], 0));  // download i - 2 of this slot pair = the one in flight
+      CK(cudaMemcpyAsync(g.bin[q], W_in[mine[L][i]], bytes, cudaMemcpyHostToDevice, g.cin));
+      CK(cudaEventRecord(g.ev_in[q], g.cin));
     };
     const int grid = h->grid_for((long long)n, 256);
-    // single domain: every iteration is one graph launch (plan + switch to
-    // the sweep of its theta), no host synchronisation inside the batch
-    const bool one_graph = !h->sharded() && h->use_graph && h->plan_graph_on && !h->ktime;
-    if (one_graph) {
-      const bool same = h->iter_graph && h->iter_opt.theta_max == opt->theta_max &&
-                        h->iter_opt.cfl == opt->cfl && h->iter_opt.dt_cap == opt->dt_cap;
-      if (!same) build_iter_graph(*h, *opt);
-      const size_t need = (size_t)n_inputs * iterations;
-      if (need > h->batch_cap) {
-        if (h->batch_plans) CK(cudaFreeHost(h->batch_plans));
-        CK(cudaMallocHost(&h->batch_plans, need * sizeof(PlanDev)));
-        h->batch_cap = need;
-      }
-    }
-    if (n_inputs > 0) upload(0);
-    for (int j = 0; j < n_inputs; ++j) {
-      const int q = j & 1;
-      if (j + 1 < n_inputs) upload(j + 1);
+    auto process = [&](int L, int i) {
+      tafv_gpu& g = *lanes[L];
+      const int j = mine[L][i];
+      const int q = i & 1;
+      if (i + 1 < (int)mine[L].size()) upload(L, i + 1);
       // state j: W from the staged input, w = W / V (kernels.cpp:237-241)
-      CK(cudaStreamWaitEvent(h->st, h->ev_in[q], 0));
-      k_load_extensive<<<grid, 256, 0, h->st>>>(h->bin[q], h->d_cperm, h->vol, h->N, h->nv, h->W, h->w);
-      CK(cudaEventRecord(h->ev_in_free[q], h->st));
-      h->t0 = 0.0;
-      h->iteration = 0;
-      h->state_set = true;
-      h->has_plan = false;
+      CK(cudaStreamWaitEvent(g.st, g.ev_in[q], 0));
+      k_load_extensive<<<grid, 256, 0, g.st>>>(g.bin[q], g.d_cperm, g.vol, g.N, g.nv, g.W, g.w);
+      CK(cudaEventRecord(g.ev_in_free[q], g.st));
+      g.t0 = 0.0;
+      g.iteration = 0;
+      g.state_set = true;
+      g.has_plan = false;
       if (one_graph) {
         for (int it = 0; it < iterations; ++it) {
-          CK(cudaGraphLaunch(h->iter_graph, h->st));
-          // this iteration's plan + its sweep's flags and totals
-          // stored by a kernel into the pinned (device-mapped) host array:
-          // a copy-engine transfer would queue behind the bulk download of
-          // the previous input on the same engine and stall this stream
-          k_store_plan<<<1, 128, 0, h->st>>>(h->dplan, &h->batch_plans[(size_t)j * iterations + it]);
+          CK(cudaGraphLaunch(g.iter_graph, g.st));
+          // this iteration's plan + its sweep's flags and totals, stored by a
+          // kernel into the pinned (device-mapped) host array: a copy-engine
+          // transfer would queue behind the bulk downloads on the same engine
+          k_store_plan<<<1, 128, 0, g.st>>>(g.dplan, &g.batch_plans[(size_t)i * iterations + it]);
         }
       } else {
-        integrate_pipelined(*h, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
+        integrate_pipelined(g, *opt, iterations, j + 1 == n_inputs ? last : nullptr, false);
       }
       // output j: W in original order -> staging -> host on the download
-      // copy stream, under input j+1's compute. (A copy-engine read-back of
-      // the plan on the library stream queued behind these downloads and
-      // stalled it; the plan now goes to the host by a kernel, store_plan.)
-      CK(cudaStreamWaitEvent(h->st, h->ev_out_free[q], 0));
-      k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[q]);
-      if (h->dl_stream) {
-        CK(cudaEventRecord(h->ev_out[q], h->st));
-        CK(cudaStreamWaitEvent(h->cout, h->ev_out[q], 0));
-        CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->cout));
-        CK(cudaEventRecord(h->ev_out_free[q], h->cout));
+      // copy stream, under the next input's compute. (A copy-engine read-back
+      // of the plan on the library stream queued behind these downloads and
+      // stalled it; the plan goes to the host by a kernel, store_plan.)
+      CK(cudaStreamWaitEvent(g.st, g.ev_out_free[q], 0));
+      k_scatter_rows<<<grid, 256, 0, g.st>>>(g.W, g.d_cperm, g.N, g.nv, g.bout[q]);
+      if (g.dl_stream) {
+        CK(cudaEventRecord(g.ev_out[q], g.st));
+        CK(cudaStreamWaitEvent(g.cout, g.ev_out[q], 0));
+        CK(cudaMemcpyAsync(W_out[j], g.bout[q], bytes, cudaMemcpyDeviceToHost, g.cout));
+        CK(cudaEventRecord(g.ev_out_free[q], g.cout));
       } else {
-        CK(cudaMemcpyAsync(W_out[j], h->bout[q], bytes, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaEventRecord(h->ev_out_free[q], h->st));
+        CK(cudaMemcpyAsync(W_out[j], g.bout[q], bytes, cudaMemcpyDeviceToHost, g.st));
+        CK(cudaEventRecord(g.ev_out_free[q], g.st));
       }
+    };
+    for (int L = 0; L < nl; ++L)
+      if (!mine[L].empty()) upload(L, 0);
+    const int rounds = n_inputs == 0 ? 0 : (int)mine[0].size();
+    for (int i = 0; i < rounds; ++i)
+      for (int L = nl - 1; L >= 0; --L)  // input order: the twin's input precedes this handle's
+        if (i < (int)mine[L].size()) process(L, i);
+    for (tafv_gpu* g : lanes) {
+      CK(cudaStreamSynchronize(g->cout));
+      CK(cudaStreamSynchronize(g->cin));
+      CK(cudaStreamSynchronize(g->st));
     }
-    CK(cudaStreamSynchronize(h->cout));
-    CK(cudaStreamSynchronize(h->cin));
-    CK(cudaStreamSynchronize(h->st));
-    if (one_graph) {  // the plans and flags of every iteration, in order
+    if (one_graph) {  // the plans and flags of every iteration, in input order
+      std::vector<int> local(n_inputs);
+      for (int L = 0; L < nl; ++L)
+        for (size_t i = 0; i < mine[L].size(); ++i) local[mine[L][i]] = (int)i;
       for (int j = 0; j < n_inputs; ++j) {
-        h->t0 = 0.0;
-        h->iteration = 0;
+        tafv_gpu& g = *lanes[lane_of(j)];
+        g.t0 = 0.0;
+        g.iteration = 0;
         for (int it = 0; it < iterations; ++it) {
-          *h->hplan = h->batch_plans[(size_t)j * iterations + it];
-          h->plan_nkeys = opt->theta_max + 1;
-          parse_plan(*h);
-          if (!(std::isfinite(h->dt) && h->dt > 0.0)) {
-            h->has_plan = false;
+          *g.hplan = g.batch_plans[(size_t)local[j] * iterations + it];
+          g.plan_nkeys = opt->theta_max + 1;
+          parse_plan(g);
+          if (!(std::isfinite(g.dt) && g.dt > 0.0)) {
+            g.has_plan = false;
             throw Error{TAFV_EINVAL, "integrate: stable step collapsed"};
           }
-          close_iteration(*h, j + 1 == n_inputs && it + 1 == iterations ? last : nullptr);
+          close_iteration(g, j + 1 == n_inputs && it + 1 == iterations ? last : nullptr);
         }
+        g.has_plan = false;
       }
-      h->has_plan = false;
     }
   });
 }
+
 
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
   return guard(h, [&] {
@@ -1976,6 +2085,8 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
 int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
   return guard(h, [&] {
     const std::string n = name ? name : "";
+    delete h->twin;  // rebuilt with the new settings by the next run_batch
+    h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
     } else if (n == "slot_geo") {
@@ -2001,6 +2112,8 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
         for (auto e : g.second.evs) cudaEventDestroy(e);
       }
       h->graphs.clear();
+    } else if (n == "batch_lanes") {
+      h->batch_lanes = (int)value;
     } else if (n == "plan_graph") {
       h->plan_graph_on = value != 0;
     } else if (n == "use_graph") {
