@@ -337,6 +337,39 @@ def test_run_batch_matches_separate_runs(gpu):
         b.run_batch([Ws[1], bad], [np.empty_like(bad), np.empty_like(bad)], cfg.options(), 2)
 
 
+def test_run_batch_two_lanes_equal_one_lane(gpu):
+    """run_batch alternates inputs between the handle and its twin (two
+    concurrent lanes): outputs bitwise equal to the one-lane batch, the last
+    record equal, and the handle's state afterwards is the last input's."""
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    a = Solver(mesh, "euler")
+    a.set_state(cfg.initial_state(mesh))
+    Ws = []
+    for _ in range(5):
+        a.reference_integrate(cfg.options(), 1)
+        Ws.append(np.ascontiguousarray(a.get_state()[1]))
+    outs = {}
+    recs = {}
+    states = {}
+    for lanes in (1, 2):
+        b = Solver(mesh, "euler")
+        b.set_flag("batch_lanes", lanes)
+        o = [np.empty_like(x) for x in Ws]
+        recs[lanes] = b.run_batch(Ws, o, cfg.options(), 3)
+        outs[lanes] = o
+        states[lanes] = b.get_state()
+        # a second batch on the same handle reuses the twin and its graphs
+        o2 = [np.empty_like(x) for x in Ws[:3]]
+        b.run_batch(Ws[:3], o2, cfg.options(), 3)
+        assert all(x.tobytes() == y.tobytes() for x, y in zip(o2, o[:3]))
+    assert all(x.tobytes() == y.tobytes() for x, y in zip(outs[1], outs[2]))
+    assert recs[1] == recs[2]
+    for x, y in zip(states[1], states[2]):
+        assert np.asarray(x).tobytes() == np.asarray(y).tobytes()
+    assert states[2][1].tobytes() == outs[2][-1].tobytes()
+
+
 def test_run_batch_sharded_loopback(gpu):
     """run_batch on 2 loopback shards (local arrays in shard order): the
     owned rows equal the single-domain batch bitwise."""
