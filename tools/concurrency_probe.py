@@ -8,7 +8,7 @@ cfg = configs.get(2); mesh = cfg.mesh(); w0 = cfg.initial_state(mesh); opt = cfg
 K = 30
 def ceff(r):
     return sum(n << (r["theta"] - l) for l, n in enumerate(r["level_cells"]))
-sol = [Solver(mesh, "euler") for _ in range(2)]
+sol = [Solver(mesh, "euler") for _ in range(3)]
 for s in sol:
     s.set_state(w0); s.reference_integrate(opt, 3)
 def work(s, out):
@@ -17,7 +17,7 @@ def work(s, out):
     t = time.perf_counter()
     recs = s.reference_integrate(opt, K)
     out.append((time.perf_counter() - t, sum(ceff(r) for r in recs)))
-for n in (1, 2, 1, 2):
+for n in (1, 2, 3, 1, 2, 3):
     outs = [[] for _ in range(n)]
     th = [threading.Thread(target=work, args=(sol[i], outs[i])) for i in range(n)]
     t = time.perf_counter()
