@@ -255,7 +255,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config generator)",
         "config": {"workload": cfg.name, "cells": cfg.n_cells, "theta_max": cfg.theta_max,
                    "cfl": cfg.cfl},
@@ -278,6 +278,9 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=40)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = the config tiled N times (one copy per GPU); strong = the config "
+                         "itself split into N slabs (e.g. --config 4 --scaling strong for the 80M-cell run)")
     ap.add_argument("--flag", action="append", default=[],
                     help="library launch knob name=value (tafv_gpu_set_flag), for A/B runs")
     args = ap.parse_args()
@@ -299,9 +302,14 @@ def main():
 
     from paper_1704_01144_b200 import Solver, configs, shard
     from paper_1704_01144_b200.api import Comm
-    # N > 1: weak scaling, config tiled N times along x, one slab (= one copy
-    # of the config) per GPU, NCCL halo exchange between slab neighbours.
-    cfg = configs.get(args.config).tiled(world)
+    # N > 1: weak scaling (default), config tiled N times along x, one slab
+    # (= one copy of the config) per GPU; or strong scaling (--scaling
+    # strong), the config itself cut into N slabs along x (perpendicular to
+    # config 4's blast wall, so the fine region spans every slab, SURVEY.md
+    # §7). NCCL halo exchange between slab neighbours either way.
+    cfg = configs.get(args.config)
+    if args.scaling == "weak":
+        cfg = cfg.tiled(world)
     mesh = cfg.mesh()
     w0 = cfg.initial_state(mesh)
     opt = cfg.options()
@@ -431,7 +439,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "plan_ms_per_step": ms_plan / args.steps,
             "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config generator: jittered/graded/permuted hex mesh, blast)",
             "config": {"workload": cfg.name, "cells": int(n), "faces": int(len(mesh["fa"])),
                        "theta_max": cfg.theta_max, "cfl": cfg.cfl,
