@@ -211,9 +211,11 @@ def test_sharded_periodic_matches_single_domain_bitwise(world, axis, gpu):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg_id,iters", [(1, 200), (2, 50)])
+@pytest.mark.parametrize("cfg_id,iters", [(1, 200), (2, 50), (3, 20)])
 def test_euler_full_size_bitwise(cfg_id, iters, gpu):
-    """Configs 1 and 2 at their full BASELINE size and iteration count."""
+    """Configs 1, 2 and 3 (8M cells, 4 levels) at their full BASELINE size and
+    iteration count: state bitwise and plan lists bit-exact every iteration
+    against the multi-threaded oracle."""
     run_pair(configs.get(cfg_id), iters, threads=os.cpu_count() or 8, check_lists=True)
 
 
