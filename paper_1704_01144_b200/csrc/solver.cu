@@ -1935,7 +1935,14 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
     const bool one_graph = !h->sharded() && h->use_graph && h->plan_graph_on && !h->ktime;
     std::vector<tafv_gpu*> lanes{h};
     if (one_graph && n_inputs >= 2 && h->batch_lanes >= 2) {
-      if (!h->twin) h->twin = make_twin(*h);
+      if (!h->twin) {
+        try {
+          h->twin = make_twin(*h);
+        } catch (const Error&) {  // no room for a second state: one lane
+          h->twin = nullptr;
+          cudaGetLastError();
+        }
+      }
       if (h->twin) lanes.push_back(h->twin);
     }
     const int nl = (int)lanes.size();
