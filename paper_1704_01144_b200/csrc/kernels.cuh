@@ -183,6 +183,9 @@ __device__ __forceinline__ double slot_sign(int e) { return e >= 0 ? 1.0 : -1.0;
 #ifndef TAFV_BJ2
 #define TAFV_BJ2 1
 #endif
+#ifndef TAFV_BJZ
+#define TAFV_BJZ 1
+#endif
 // Barth-Jespersen update alpha = min(alpha, minmod(delta, head) / delta)
 // (kernels.cpp:111-117) with the division evaluated only where its value can
 // matter. Exactly equivalent, including signed zeros and NaN:
@@ -204,7 +207,16 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
   const double A = pos ? hp : hn;
   const bool aok = A > 0.0;
   const double ad = fabs(delta);
+#if TAFV_BJZ
+  // the zero outcome as word selects: smin(alpha, +-0) is +-0 exactly when
+  // alpha > 0 (alpha is never negative), and +-0 has a zero low word
+  const bool upd = (pos || neg) && !aok && alpha > 0.0;
+  const int hi = upd ? (neg ? (int)0x80000000 : 0) : __double2hiint(alpha);
+  const int lo = upd ? 0 : __double2loint(alpha);
+  alpha = __hiloint2double(hi, lo);
+#else
   if ((pos || neg) && !aok) alpha = smin(alpha, pos ? 0.0 : -0.0);
+#endif
   if (aok && ad > A) alpha = smin(alpha, A / ad);
   return alpha;
 #else
