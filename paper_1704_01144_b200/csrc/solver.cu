@@ -128,6 +128,10 @@ struct tafv_gpu {
   bool capturing = false;
   int grid_k1 = 0, grid_k2 = 0, grid_k3 = 0;
   int plan_nkeys = 0;
+  // single-domain plans fuse the ilogb classification into the first Jacobi
+  // sweep, so raw levels live only in registers; get_array("raw_level")
+  // recomputes them (k_classify, the same function) while this is set
+  bool raw_lazy = false;
   int* adj_off = nullptr;
   int* adj_face = nullptr;  // [M] face id, ~f on the face's right side
   int* adj_nb = nullptr;    // [M] neighbour cell or -1
@@ -1025,7 +1029,17 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt);
 
 // plan_iteration on the device: either the captured plan graph of these
 // options (kernels + the read-back copy, one launch) or direct launches.
+// Raw levels of the last regular plan from its dt_max and dt_min (bitwise the
+// values the fused sweep used: the same classify_raw on the same operands).
+void materialise_raw(tafv_gpu& h) {
+  k_classify<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.N, h.dtmax, h.dplan, h.plan_nkeys - 1, h.raw);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h.st));
+  h.raw_lazy = false;
+}
+
 void enqueue_plan(tafv_gpu& h, const tafv_options& opt) {
+  h.raw_lazy = !h.sharded();  // single domain: raw levels fused away (materialised on read)
   const Range r("tafv.plan");
   require(opt.theta_max >= 0, "classify: theta_max must be >= 0");
   require(opt.theta_max < kMaxLevels, "classify: theta_max above the supported 15");
@@ -1134,6 +1148,9 @@ void plan(tafv_gpu& h, const tafv_options& opt) {
 }
 
 void inject(tafv_gpu& h, const int32_t* tau_in, double dt, const tafv_options* opt) {
+  // the reference leaves raw_level as the last plan_iteration computed it:
+  // materialise it before dt_max / dt_min are overwritten
+  if (h.raw_lazy) materialise_raw(h);
   require(h.state_set || dt > 0.0, "inject_levels: state not set");
   // shards take the GLOBAL level map and keep their local cells' entries
   std::vector<int32_t> local;
@@ -2075,6 +2092,7 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
       cudaFree(win);
     }
     else if (n == "raw_level" || n == "tau") {
+      if (n == "raw_level" && h->raw_lazy) materialise_raw(*h);
       std::vector<int8_t> v(h->N);
       CK(cudaMemcpy(v.data(), n == "tau" ? h->tau : h->raw, h->N, cudaMemcpyDeviceToHost));
       int32_t* o = static_cast<int32_t*>(out);

@@ -686,3 +686,30 @@ def test_sharded_repartition_by_level_cost_bitwise(gpu):
     g.reference_integrate(cfg.options(), n1 + n2)
     np.testing.assert_array_equal(w, g.get_state()[0])
     assert out[0][3] == n1 + n2
+
+
+def test_raw_levels_and_dt_max_arrays(gpu):
+    """SolverState::raw_level and dt_max (state.hpp:17-50) read back after a
+    plan equal the oracle's bitwise (the single-domain plan fuses the
+    classification into its first smoothing sweep; the raw levels are
+    materialised on read), and an injected plan leaves raw_level as the last
+    plan_iteration computed it, as in the reference."""
+    from oracle import OracleSolver
+    cfg = configs.get(2, 5)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    o = OracleSolver(mesh, "euler")
+    o.init_values(w0.reshape(-1))
+    o.set_options(opt.theta_max, opt.cfl, opt.dt_cap)
+    g.plan_iteration(opt)
+    o.plan_iteration()
+    raw = g.get_array("raw_level")
+    assert (raw == o.get("raw_level")).all() and raw.max() >= 1
+    assert g.get_array("dt_max").tobytes() == o.get("dt_max").tobytes()
+    g.run_iteration()
+    tau = g.get_array("tau")
+    g.inject_levels(np.zeros_like(tau), 1e-6, opt)
+    assert (g.get_array("raw_level") == raw).all()

@@ -163,3 +163,28 @@ def test_iterations_end_synchronous_with_consistent_extensive_values(gpu):
         assert (w.reshape(-1) == W.reshape(-1) / mesh["vol"]).all()
         assert r["t_start"] == t and t0 == t + r["dt"] * (1 << r["theta"])
         t = t0
+
+
+def _plan_levels(mesh, chl, theta_max):
+    """(raw, smoothed) levels the device plan assigns (dt_max classification,
+    then Jacobi smoothing) for cell stable steps proportional to `chl`
+    (advection at unit speed)."""
+    m = dict(mesh)
+    m["chl"] = np.asarray(chl, dtype=np.float64)
+    s = Solver(m, "advection", a=(1.0, 0.0))
+    s.set_state(np.ones(len(m["vol"])))
+    s.plan_iteration(SolverOptions(theta_max=theta_max, cfl=0.5, dt_cap=1e30))
+    return list(s.get_array("raw_level")), list(s.plan_lists()["tau"])
+
+
+def test_classification_and_smoothing_kats(gpu):
+    """test_levels.cpp:36-66 on the device plan: raw levels floor(log2 of the
+    dt ratio) clamped to theta_max (ratios 5 -> 2, 1 -> 0, 3 -> 1, 1024 -> 3),
+    and Jacobi smoothing [0,3,3] -> [0,1,2] on a line, [0,3,3,3] ->
+    [0,1,2,1] across the periodic wrap."""
+    for ratio, level in ((5.0, 2), (1.0, 0), (3.0, 1), (1024.0, 3)):
+        raw, _ = _plan_levels(line_mesh(2), [1.0, ratio], 3)
+        assert raw == [0, level], ratio
+    assert _plan_levels(line_mesh(3), [1.0, 8.0, 8.0], 3) == ([0, 3, 3], [0, 1, 2])
+    assert _plan_levels(line_mesh(4, periodic=True), [1.0, 8.0, 8.0, 8.0], 3) == ([0, 3, 3, 3], [0, 1, 2, 1])
+    assert _plan_levels(line_mesh(3), [1.0, 1.0, 1.0], 4) == ([0, 0, 0], [0, 0, 0])
