@@ -2048,6 +2048,7 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
           close_iteration(g, j + 1 == n_inputs && it + 1 == iterations ? last : nullptr);
         }
         g.has_plan = false;
+        g.raw_lazy = true;  // the last plan's raw levels, materialised on read
       }
     }
   });
