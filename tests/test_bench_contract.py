@@ -6,6 +6,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -29,3 +31,24 @@ def test_reference_arm_line_contract():
     lib = d.get("reference_library_scalar2d")
     if lib is not None:  # the unmodified reference library (oracle/_ref) when it was built
         assert lib["sequential"]["value"] > 0 and lib["task_engine"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line_contract(gpu):
+    """The GPU arm's line: contract keys, roofline / e2e / clocks objects, a
+    positive launch count and the timing rules (warm-up >= 3)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                          "--e2e-steps", "4", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads([l for l in out.stdout.strip().splitlines() if l.startswith("{")][-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+        assert k in d, k
+    assert d["value"] > 0 and d["warmup"] >= 3 and d["gpu_launches"] > 0 and "impl" not in d
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-3)
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == e["d2h_bytes_per_step"] == 40 * d["config"]["cells"]
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert "l2" in d["config"] and d["config"]["workload"].startswith("cfg2")
