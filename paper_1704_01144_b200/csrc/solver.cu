@@ -13,7 +13,15 @@
 //   * per-iteration plan: int8 levels/cadences and level-sorted index lists
 //     whose prefixes are the active sets of every subiteration level.
 // One plan read-back per iteration (theta, counts, dt: the host needs theta
-// to size the 2^theta sweep); everything else stays on the device.
+// to size the 2^theta sweep), stored by a kernel into mapped pinned memory
+// (store_plan); everything else stays on the device.
+//
+// Streams: the library stream `st` carries the plan and sweep graphs; a
+// shard's halo exchange runs on a high-priority comm stream `cst` under the
+// next phase's K1/K2 over the deep cells / interior faces (halo_rows /
+// halo_join); run_batch adds copy streams per lane and a twin handle (a
+// second state over the same mesh arrays) so two inputs advance
+// concurrently.
 
 #include <cuda_runtime.h>
 #include <nccl.h>
