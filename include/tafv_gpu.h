@@ -162,9 +162,11 @@ int tafv_gpu_run_iteration(tafv_gpu* h, tafv_record* out);
  * n x {plan_iteration, run_iteration}; out has room for n records. */
 int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* out);
 
-/* Same as tafv_gpu_iterate but without per-iteration records or the
- * per-iteration host wait for them (records of the last iteration only);
- * the device-resident throughput path. */
+/* Same as tafv_gpu_iterate but keeps only the record of the LAST iteration.
+ * The host still synchronises once per iteration (one pinned read-back
+ * carries the next plan -- its theta picks the next sweep graph -- and the
+ * divergence flag), exactly as tafv_gpu_iterate does; the state never
+ * leaves the device. */
 int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* last);
 
 /* A batch of independent inputs (ensemble members, restarts): for each
@@ -177,6 +179,17 @@ int tafv_gpu_advance(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_recor
  * arrays hold the rank's local cells in the order of its shard cell list. */
 int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, int32_t iterations,
                        const double* const* W_in, double* const* W_out, tafv_record* last);
+
+/* reference_integrate (reference.cpp:135-142) on a HOST-resident state:
+ * the caller's SolverState (state.hpp:17-50) stays in host memory and every
+ * iteration crosses the link both ways -- W uploaded from W_host (w = W / V
+ * on the device, the relation every corrector leaves, kernels.cpp:237-241),
+ * plan_iteration + run_iteration, the new W written back into W_host before
+ * the next upload (chunked, so the two directions overlap). W_host: extensive
+ * rows in original cell order (shards: local cells in shard order); pass
+ * pinned memory. out has room for n records. Bitwise equal to
+ * tafv_gpu_iterate from set_state(NULL, W). */
+int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, double* W_host, tafv_record* out);
 
 /* Debug/parity access to intermediate SolverState arrays in original ids:
  * "w_pred" [nc][nv], "grad" [nc][nv][3], "phi_pred" / "int_substep" /
@@ -223,6 +236,11 @@ int tafv_shard_describe(const tafv_mesh_view* mesh, const int32_t* rank_of_cell,
                         int32_t* peers, int32_t* send_counts, int32_t* recv_counts,
                         int32_t* send_flat, int32_t* recv_flat);
 const char* tafv_shard_last_error(void);
+
+/* smooth_to_fixpoint (levels.cpp:33-51) on the host, in place: the slab cut
+ * weights of a decomposed run come from the initial plan's levels before
+ * any device is set up (DistDriver::repartition, exchange.cpp:598-603). */
+int tafv_level_smooth(const tafv_mesh_view* mesh, int32_t* tau);
 
 /* ---- multi-GPU ranks -------------------------------------------------------
  * A communicator replaces the reference's Transport + RankComm
@@ -279,6 +297,20 @@ int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* x, const dou
                   double* cell_char_length, int32_t* face_left, int32_t* face_right,
                   int32_t* face_partner, double* face_normal, double* face_area,
                   double* face_centroid);
+
+/* The cells [box6[0], box6[1]) x [box6[2], box6[3]) x [box6[4], box6[5]) of
+ * the tafv_mesh_hex lattice (nx, ny, nz, xs, ys, zs, jitter, seed; no
+ * permutation): every node -- jitter included -- sits exactly where the full
+ * mesh puts it, so the window's cells are bitwise the full mesh's cells
+ * there; faces on the window's sides become transmissive boundary faces.
+ * Bounded samples of a config (CPU baselines) and per-rank slabs. Same
+ * two-call protocol. */
+int tafv_mesh_hex_window(int32_t nx, int32_t ny, int32_t nz, const double* xs, const double* ys,
+                         const double* zs, const int32_t* box6, double jitter, uint64_t seed,
+                         int32_t* n_cells, int32_t* n_faces, double* cell_volume, double* cell_centroid,
+                         double* cell_char_length, int32_t* face_left, int32_t* face_right,
+                         int32_t* face_partner, double* face_normal, double* face_area,
+                         double* face_centroid);
 
 #ifdef __cplusplus
 }

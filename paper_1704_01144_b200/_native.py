@@ -103,9 +103,9 @@ class PlanInfo(C.Structure):
 EXPORTS = [
     "tafv_gpu_create", "tafv_gpu_destroy", "tafv_gpu_last_error", "tafv_gpu_set_state",
     "tafv_gpu_get_state", "tafv_gpu_plan", "tafv_gpu_inject_levels", "tafv_gpu_get_plan_lists",
-    "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_run_batch", "tafv_gpu_get_array",
-    "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex",
-    "tafv_partition_slabs", "tafv_shard_describe", "tafv_shard_last_error",
+    "tafv_gpu_run_iteration", "tafv_gpu_iterate", "tafv_gpu_advance", "tafv_gpu_run_batch", "tafv_gpu_iterate_host", "tafv_gpu_get_array",
+    "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex", "tafv_mesh_hex_window",
+    "tafv_partition_slabs", "tafv_shard_describe", "tafv_level_smooth", "tafv_shard_last_error",
     "tafv_comm_nccl_unique_id", "tafv_comm_create_nccl", "tafv_comm_create_loopback",
     "tafv_comm_destroy", "tafv_gpu_create_shard",
     "tafv_mesh_save", "tafv_mesh_load", "tafv_mesh_hash", "tafv_snapshot_save", "tafv_snapshot_load",
@@ -113,6 +113,18 @@ EXPORTS = [
 ]
 
 _lib = None
+
+
+def bind_meshgen(L):
+    """argtypes of the mesh generator entry points (csrc/meshgen.cpp), which
+    the CPU checker library (oracle/) also compiles in, so a reference-arm
+    process can build a config's mesh without mapping this library."""
+    vp, i32, dbl = C.c_void_p, C.c_int32, C.c_double
+    L.tafv_mesh_hex.argtypes = [i32, i32, i32, vp, vp, vp, dbl, C.c_uint64, i32,
+                                C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    L.tafv_mesh_hex_window.argtypes = [i32, i32, i32, vp, vp, vp, vp, dbl, C.c_uint64,
+                                       C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    return L
 
 
 def lib():
@@ -129,6 +141,7 @@ def lib():
     L.tafv_gpu_last_error.argtypes = [vp]
     L.tafv_gpu_last_error.restype = C.c_char_p
     L.tafv_gpu_run_batch.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+    L.tafv_gpu_iterate_host.argtypes = [vp, C.POINTER(Options), i32, vp, vp]
     L.tafv_gpu_set_state.argtypes = [vp, vp, vp, dbl, i32]
     L.tafv_gpu_get_state.argtypes = [vp, vp, vp, C.POINTER(dbl), C.POINTER(i32)]
     L.tafv_gpu_plan.argtypes = [vp, C.POINTER(Options), C.POINTER(PlanInfo)]
@@ -142,10 +155,10 @@ def lib():
     L.tafv_gpu_stats.argtypes = [vp, C.POINTER(i64), vp]
     L.tafv_gpu_kernel_times.argtypes = [vp, vp, vp, vp]
     L.tafv_gpu_mesh_info.argtypes = [vp, vp]
-    L.tafv_mesh_hex.argtypes = [i32, i32, i32, vp, vp, vp, dbl, C.c_uint64, i32,
-                                C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
+    bind_meshgen(L)
     L.tafv_partition_slabs.argtypes = [C.POINTER(MeshView), i32, i32, vp, vp]
     L.tafv_shard_describe.argtypes = [C.POINTER(MeshView), vp, i32, i32] + [vp] * 8
+    L.tafv_level_smooth.argtypes = [C.POINTER(MeshView), vp]
     L.tafv_shard_last_error.restype = C.c_char_p
     L.tafv_comm_nccl_unique_id.argtypes = [vp]
     L.tafv_comm_create_nccl.argtypes = [vp, i32, i32, C.c_int, C.POINTER(vp)]

@@ -214,9 +214,21 @@ class Solver:
         # a shard's arrays hold its local cells (shard.describe()["cells"] order)
         rows = self.mesh_info()["n_cells"] if hasattr(self, "rank") else self.nc
         for a in list(W_in) + list(W_out):
-            size = a.numel() if hasattr(a, "numel") else a.size
-            if size != rows * self.nv:
-                raise InvalidArgument("run_batch: wrong buffer size")
+            # the library copies rows*nv*8 bytes through the raw pointer: only
+            # C-contiguous float64 HOST buffers of exactly that size are safe
+            if hasattr(a, "data_ptr"):  # torch tensor
+                import torch
+                ok = (a.dtype == torch.float64 and a.is_contiguous() and a.device.type == "cpu"
+                      and a.numel() == rows * self.nv)
+            else:
+                ok = (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous
+                      and a.size == rows * self.nv)
+            if not ok:
+                raise InvalidArgument("run_batch: buffers must be C-contiguous float64 host arrays of "
+                                      f"{rows} x {self.nv} values")
+        for a in W_out:
+            if not (a.flags.writeable if isinstance(a, np.ndarray) else True):
+                raise InvalidArgument("run_batch: output buffer is read-only")
         pin = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_in])
         pout = (C.c_void_p * max(1, n))(*[ptr(a) for a in W_out])
         rec = N.Record()
@@ -224,6 +236,29 @@ class Solver:
                                            C.byref(rec)))
         self._plan = None
         return rec.as_dict()
+
+    def iterate_host(self, W_host, opt: SolverOptions, n=1):
+        """tafv_gpu_iterate_host: reference_integrate with the state held in
+        the caller's HOST buffer W_host (extensive rows, original cell order;
+        a shard: its local cells in shard.describe()["cells"] order), which
+        every iteration uploads and receives the new W. Returns the records."""
+        rows = self.mesh_info()["n_cells"] if hasattr(self, "rank") else self.nc
+        if hasattr(W_host, "data_ptr"):
+            import torch
+            ok = (W_host.dtype == torch.float64 and W_host.is_contiguous() and W_host.device.type == "cpu"
+                  and W_host.numel() == rows * self.nv)
+            p = W_host.data_ptr()
+        else:
+            ok = (isinstance(W_host, np.ndarray) and W_host.dtype == np.float64 and W_host.flags.c_contiguous
+                  and W_host.flags.writeable and W_host.size == rows * self.nv)
+            p = W_host.ctypes.data if ok else None
+        if not ok:
+            raise InvalidArgument("iterate_host: W_host must be a writable C-contiguous float64 host array of "
+                                  f"{rows} x {self.nv} values")
+        recs = (N.Record * max(1, n))()
+        self._c(self.lib.tafv_gpu_iterate_host(self.h, C.byref(opt.c()), int(n), C.c_void_p(p), recs))
+        self._plan = None
+        return [recs[i].as_dict() for i in range(n)]
 
     def get_array(self, name):
         if name in ("raw_level", "tau"):

@@ -64,6 +64,11 @@ class Config:
     def n_cells(self):
         return int(np.prod(self.n))
 
+    @property
+    def n_faces(self):
+        nx, ny, nz = self.n
+        return int((nx + 1) * ny * nz + nx * (ny + 1) * nz + nx * ny * (nz + 1))
+
     def nodes(self):
         axes = []
         for d, n in enumerate(self.n):
@@ -86,9 +91,17 @@ class Config:
             return meshgen.geometric_nodes(n, a[0]) if d == 2 else meshgen.uniform_nodes(n)
         raise ValueError(g)
 
-    def mesh(self):
+    def mesh(self, window=None, lib=None):
+        """The config's mesh; `window` = (i0, i1, j0, j1, k0, k1) gives only
+        those cells (bitwise the full mesh's cells there, cut sides
+        transmissive): bounded samples and slabs. `lib`: the library whose
+        generator runs (default the product's; the CPU checkers pass the
+        oracle library so a CPU-only process never maps the product)."""
+        if window is not None and self.permute:
+            raise ValueError("mesh: windows of permuted configs are not supported")
         x, y, z = self.nodes()
-        m = meshgen.hex_mesh(x, y, z, jitter=self.jitter, seed=self.seed, permute=self.permute)
+        m = meshgen.hex_mesh(x, y, z, jitter=self.jitter, seed=self.seed, permute=self.permute,
+                             window=window, lib=lib)
         return meshgen.make_periodic(m, self.periodic) if self.periodic else m
 
     def initial_state(self, mesh):

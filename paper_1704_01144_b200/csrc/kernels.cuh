@@ -1051,7 +1051,18 @@ __global__ void k_window_rows(const double* iwin, const double* isub, const uint
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long row = i / width, j = row * stride + i % width;
-    dst[i] = alias[row] ? isub[j] + 0.0 : iwin[j];
+    dst[i] = alias && alias[row] ? isub[j] + 0.0 : iwin[j];
+  }
+}
+
+// iwin_alias switched off: faces still aliased get their window materialised
+// (0.0 + int_substep, what K2 would have accumulated) and lose the alias.
+__global__ void k_materialise_alias(double* iwin, const double* isub, uint8_t* alias, int n, int nv,
+                                    int stride) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+    if (!alias[f]) continue;
+    for (int k = 0; k < nv; ++k) iwin[(size_t)f * stride + k] = 0.0 + isub[(size_t)f * stride + k];
+    alias[f] = 0;
   }
 }
 

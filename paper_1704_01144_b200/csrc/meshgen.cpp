@@ -89,16 +89,27 @@ inline Quad quad(V3 p0, V3 p1, V3 p2, V3 p3) {
 
 }  // namespace
 
-extern "C" int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* xs,
-                             const double* ys, const double* zs, double jitter, uint64_t seed,
-                             int32_t permute, int32_t* n_cells, int32_t* n_faces,
-                             double* cell_volume, double* cell_centroid, double* cell_char_length,
-                             int32_t* face_left, int32_t* face_right, int32_t* face_partner,
-                             double* face_normal, double* face_area, double* face_centroid) {
+// The cells [i0, i1) x [j0, j1) x [k0, k1) of the global nx x ny x nz
+// lattice on nodes xs[nx+1], ys[ny+1], zs[nz+1]: node positions (jitter key,
+// local spacing, "interior" = not on the GLOBAL box) are those of the full
+// mesh, so a window's cells are bitwise the full mesh's cells there. Faces
+// on the window's sides that are interior in the full mesh become boundary
+// faces (transmissive) of the window mesh. The full mesh is the window
+// [0, nx) x [0, ny) x [0, nz); only it may be permuted.
+static int hex_window(int32_t nx, int32_t ny, int32_t nz, const double* xs, const double* ys, const double* zs,
+               const int32_t* box, double jitter, uint64_t seed, int32_t permute, int32_t* n_cells,
+               int32_t* n_faces, double* cell_volume, double* cell_centroid, double* cell_char_length,
+               int32_t* face_left, int32_t* face_right, int32_t* face_partner, double* face_normal,
+               double* face_area, double* face_centroid) {
   if (nx < 1 || ny < 1 || nz < 1) return TAFV_EINVAL;
-  const int64_t N = int64_t(nx) * ny * nz;
-  const int64_t Fx = int64_t(nx + 1) * ny * nz, Fy = int64_t(nx) * (ny + 1) * nz,
-                Fz = int64_t(nx) * ny * (nz + 1);
+  const int64_t i0 = box[0], j0 = box[2], k0 = box[4];
+  const int64_t wx = int64_t(box[1]) - i0, wy = int64_t(box[3]) - j0, wz = int64_t(box[5]) - k0;
+  if (i0 < 0 || j0 < 0 || k0 < 0 || wx < 1 || wy < 1 || wz < 1 || i0 + wx > nx || j0 + wy > ny ||
+      k0 + wz > nz)
+    return TAFV_EINVAL;
+  if (permute && (wx != nx || wy != ny || wz != nz)) return TAFV_EINVAL;
+  const int64_t N = wx * wy * wz;
+  const int64_t Fx = (wx + 1) * wy * wz, Fy = wx * (wy + 1) * wz, Fz = wx * wy * (wz + 1);
   const int64_t F = Fx + Fy + Fz;
   if (N > INT32_MAX || F > INT32_MAX) return TAFV_EINVAL;
   if (n_cells) *n_cells = static_cast<int32_t>(N);
@@ -111,27 +122,31 @@ extern "C" int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* x
   for (int i = 0; i < nz; ++i)
     if (!(zs[i + 1] > zs[i])) return TAFV_EINVAL;
 
-  // Node lattice with jitter.
-  const int64_t NX = nx + 1, NY = ny + 1, NZ = nz + 1;
+  // Node lattice of the window with the full mesh's jitter (global keys).
+  const int64_t GX = nx + 1, GY = ny + 1;
+  const int64_t NX = wx + 1, NY = wy + 1, NZ = wz + 1;
   std::vector<V3> node(NX * NY * NZ);
-  auto nid = [&](int64_t i, int64_t j, int64_t k) { return (k * NY + j) * NX + i; };
+  auto nid = [&](int64_t i, int64_t j, int64_t k) { return (k * NY + j) * NX + i; };  // window-local
   auto local = [](const double* a, int64_t i) { return std::min(a[i] - a[i - 1], a[i + 1] - a[i]); };
-  parallel(NZ, [&](int64_t k0, int64_t k1) {
-    for (int64_t k = k0; k < k1; ++k)
+  parallel(NZ, [&](int64_t a0, int64_t a1) {
+    for (int64_t k = a0; k < a1; ++k)
       for (int64_t j = 0; j < NY; ++j)
         for (int64_t i = 0; i < NX; ++i) {
-          V3 p{xs[i], ys[j], zs[k]};
-          const bool interior = i > 0 && i < nx && j > 0 && j < ny && k > 0 && k < nz;
+          const int64_t gi = i0 + i, gj = j0 + j, gk = k0 + k;
+          V3 p{xs[gi], ys[gj], zs[gk]};
+          const bool interior = gi > 0 && gi < nx && gj > 0 && gj < ny && gk > 0 && gk < nz;
           if (interior && jitter != 0.0) {
-            const uint64_t key = static_cast<uint64_t>(nid(i, j, k)) * 3;
-            p.x += jitter * local(xs, i) * (2.0 * u01(seed, key) - 1.0);
-            p.y += jitter * local(ys, j) * (2.0 * u01(seed, key + 1) - 1.0);
-            p.z += jitter * local(zs, k) * (2.0 * u01(seed, key + 2) - 1.0);
+            const uint64_t key = static_cast<uint64_t>((gk * GY + gj) * GX + gi) * 3;
+            p.x += jitter * local(xs, gi) * (2.0 * u01(seed, key) - 1.0);
+            p.y += jitter * local(ys, gj) * (2.0 * u01(seed, key + 1) - 1.0);
+            p.z += jitter * local(zs, gk) * (2.0 * u01(seed, key + 2) - 1.0);
           }
           node[nid(i, j, k)] = p;
         }
   });
-
+  nx = static_cast<int32_t>(wx);  // from here on: the window's own lattice
+  ny = static_cast<int32_t>(wy);
+  nz = static_cast<int32_t>(wz);
   std::vector<int32_t> cperm, fperm;
   if (permute) {
     cperm = shuffled(N, splitmix64(seed ^ 0xC3115ull));
@@ -238,4 +253,28 @@ extern "C" int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* x
         }
   });
   return TAFV_OK;
+}
+
+extern "C" int tafv_mesh_hex(int32_t nx, int32_t ny, int32_t nz, const double* xs,
+                             const double* ys, const double* zs, double jitter, uint64_t seed,
+                             int32_t permute, int32_t* n_cells, int32_t* n_faces,
+                             double* cell_volume, double* cell_centroid, double* cell_char_length,
+                             int32_t* face_left, int32_t* face_right, int32_t* face_partner,
+                             double* face_normal, double* face_area, double* face_centroid) {
+  const int32_t box[6] = {0, nx, 0, ny, 0, nz};
+  return hex_window(nx, ny, nz, xs, ys, zs, box, jitter, seed, permute, n_cells, n_faces, cell_volume,
+                    cell_centroid, cell_char_length, face_left, face_right, face_partner, face_normal,
+                    face_area, face_centroid);
+}
+
+extern "C" int tafv_mesh_hex_window(int32_t nx, int32_t ny, int32_t nz, const double* xs, const double* ys,
+                                    const double* zs, const int32_t* box6, double jitter, uint64_t seed,
+                                    int32_t* n_cells, int32_t* n_faces, double* cell_volume,
+                                    double* cell_centroid, double* cell_char_length, int32_t* face_left,
+                                    int32_t* face_right, int32_t* face_partner, double* face_normal,
+                                    double* face_area, double* face_centroid) {
+  if (!box6) return TAFV_EINVAL;
+  return hex_window(nx, ny, nz, xs, ys, zs, box6, jitter, seed, 0, n_cells, n_faces, cell_volume,
+                    cell_centroid, cell_char_length, face_left, face_right, face_partner, face_normal,
+                    face_area, face_centroid);
 }

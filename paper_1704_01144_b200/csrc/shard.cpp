@@ -227,4 +227,37 @@ extern "C" int tafv_shard_describe(const tafv_mesh_view* m, const int32_t* rank_
   }
 }
 
+// smooth_sweep / smooth_to_fixpoint (levels.cpp:33-51) on the host: Jacobi
+// tau <- min(tau, 1 + min over face neighbours) until no change (resolved
+// right across periodic links). Used for the slab cut weights of a
+// decomposed run (the initial plan's levels, before any device exists) and
+// for synthetic level maps.
+extern "C" int tafv_level_smooth(const tafv_mesh_view* m, int32_t* tau) {
+  try {
+    if (!m || !tau) throw std::invalid_argument("level_smooth: null argument");
+    const int N = m->n_cells, F = m->n_faces;
+    std::vector<int32_t> next(tau, tau + N);
+    for (;;) {
+      for (int f = 0; f < F; ++f) {
+        const int l = m->face_left[f];
+        const int r = m->face_right[f] >= 0 ? m->face_right[f]
+                      : m->face_partner[f] >= 0 ? m->face_left[m->face_partner[f]] : -1;
+        if (r < 0) continue;
+        next[l] = std::min(next[l], tau[r] + 1);
+        next[r] = std::min(next[r], tau[l] + 1);
+      }
+      bool changed = false;
+      for (int c = 0; c < N; ++c)
+        if (next[c] != tau[c]) {
+          changed = true;
+          tau[c] = next[c];
+        }
+      if (!changed) return TAFV_OK;
+    }
+  } catch (const std::exception& e) {
+    g_shard_err = e.what();
+    return TAFV_EINVAL;
+  }
+}
+
 extern "C" const char* tafv_shard_last_error() { return g_shard_err.c_str(); }

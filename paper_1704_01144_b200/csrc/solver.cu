@@ -186,6 +186,7 @@ struct tafv_gpu {
   double* bin[2] = {nullptr, nullptr};
   double* bout[2] = {nullptr, nullptr};
   cudaEvent_t ev_in[2] = {}, ev_in_free[2] = {}, ev_out[2] = {}, ev_out_free[2] = {};
+  std::vector<cudaEvent_t> ev_chunk;  // iterate_host: per-chunk "download landed" events
   // one-graph iteration (build_iter_graph) and its per-iteration plan copies
   cudaGraphExec_t iter_graph = nullptr;
   cudaGraphConditionalHandle iter_cond{};
@@ -315,6 +316,7 @@ struct tafv_gpu {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : evpool) cudaEventDestroy(e);
+    for (auto& e : ev_chunk) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
     if (cst) cudaStreamDestroy(cst);
     if (ev_pack) cudaEventDestroy(ev_pack);
@@ -2026,12 +2028,24 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
         CK(cudaEventRecord(g.ev_out_free[q], g.st));
       }
     };
-    for (int L = 0; L < nl; ++L)
-      if (!mine[L].empty()) upload(L, 0);
-    const int rounds = n_inputs == 0 ? 0 : (int)mine[0].size();
-    for (int i = 0; i < rounds; ++i)
-      for (int L = nl - 1; L >= 0; --L)  // input order: the twin's input precedes this handle's
-        if (i < (int)mine[L].size()) process(L, i);
+    try {
+      for (int L = 0; L < nl; ++L)
+        if (!mine[L].empty()) upload(L, 0);
+      const int rounds = n_inputs == 0 ? 0 : (int)mine[0].size();
+      for (int i = 0; i < rounds; ++i)
+        for (int L = nl - 1; L >= 0; --L)  // input order: the twin's input precedes this handle's
+          if (i < (int)mine[L].size()) process(L, i);
+    } catch (...) {
+      // copies from / into the CALLER's buffers may still be in flight on
+      // the copy streams: drain every lane before the error reaches the
+      // caller (who may free or reuse those buffers at once); secondary
+      // errors are dropped, the first one is reported
+      for (tafv_gpu* g : lanes)
+        for (cudaStream_t q : {g->cin, g->cout, g->st})
+          if (q) cudaStreamSynchronize(q);
+      cudaGetLastError();
+      throw;
+    }
     for (tafv_gpu* g : lanes) {
       CK(cudaStreamSynchronize(g->cout));
       CK(cudaStreamSynchronize(g->cin));
@@ -2062,6 +2076,71 @@ int tafv_gpu_run_batch(tafv_gpu* h, const tafv_options* opt, int32_t n_inputs, i
   });
 }
 
+
+// reference_integrate on a HOST-resident state (the caller's SolverState,
+// state.hpp:17-50, kept on the host between iterations): every iteration
+// uploads W from the caller's buffer (w = W / V on the device), runs one
+// plan + sweep, and writes the new W back into the same buffer. The copies
+// are chunked: chunk c of iteration i+1's upload starts as soon as chunk c
+// of iteration i's download has landed in the host buffer, so the two
+// directions of the link overlap (the bytes still make the full round trip
+// through the caller's memory every iteration). W_host in the batch layout
+// (original cell order; shards: local cells in shard order).
+int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, double* W_host, tafv_record* out) {
+  return guard(h, [&] {
+    require(opt != nullptr && W_host != nullptr, "iterate_host: null argument");
+    require(n >= 0, "integrate: negative iteration count");
+    batch_setup(*h, *opt, 0, false);
+    const size_t total = (size_t)h->N * h->nv;
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(total, (size_t)8 << 20));  // 64 MB
+    const int nchunks = (int)((total + chunk - 1) / chunk);
+    while ((int)h->ev_chunk.size() < nchunks) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, h->cout));  // initially complete
+      h->ev_chunk.push_back(e);
+    }
+    const int grid = h->grid_for((long long)total, 256);
+    h->ms[0] = h->ms[1] = h->ms[2] = 0.0;
+    h->launches = 0;
+    try {
+      for (int it = 0; it < n; ++it) {
+        for (int c = 0; c < nchunks; ++c) {  // upload chunk c once its previous download landed
+          const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
+          CK(cudaStreamWaitEvent(h->cin, h->ev_chunk[c], 0));
+          CK(cudaMemcpyAsync(h->bin[0] + a, W_host + a, len * sizeof(double), cudaMemcpyHostToDevice, h->cin));
+        }
+        CK(cudaEventRecord(h->ev_in[0], h->cin));
+        CK(cudaStreamWaitEvent(h->st, h->ev_in[0], 0));
+        k_load_extensive<<<grid, 256, 0, h->st>>>(h->bin[0], h->d_cperm, h->vol, h->N, h->nv, h->W, h->w);
+        CK(cudaGetLastError());
+        h->state_set = true;
+        h->has_plan = false;
+        const int64_t l0 = h->launches;
+        double ms0[3] = {h->ms[0], h->ms[1], h->ms[2]};
+        timed_call(*h, [&] { integrate_pipelined(*h, *opt, 1, out ? out + it : nullptr, true); });
+        for (int q = 0; q < 3; ++q) h->ms[q] += ms0[q];
+        h->launches += l0;
+        k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[0]);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev_out[0], h->st));
+        CK(cudaStreamWaitEvent(h->cout, h->ev_out[0], 0));
+        for (int c = 0; c < nchunks; ++c) {
+          const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
+          CK(cudaMemcpyAsync(W_host + a, h->bout[0] + a, len * sizeof(double), cudaMemcpyDeviceToHost, h->cout));
+          CK(cudaEventRecord(h->ev_chunk[c], h->cout));
+        }
+      }
+      CK(cudaStreamSynchronize(h->cout));
+    } catch (...) {
+      // the caller's buffer may still be the target of a copy in flight
+      for (cudaStream_t q : {h->cin, h->cout, h->st})
+        if (q) cudaStreamSynchronize(q);
+      cudaGetLastError();
+      throw;
+    }
+  });
+}
 
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
   return guard(h, [&] {
@@ -2095,7 +2174,8 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     }
     else if (n == "int_window") {
       double* win = dalloc<double>((size_t)h->F * h->nv);
-      k_window_rows<<<h->grid_for((long long)h->F * h->nv, 256), 256, 0, h->st>>>(h->iwin, h->isub, h->ialias,
+      k_window_rows<<<h->grid_for((long long)h->F * h->nv, 256), 256, 0, h->st>>>(h->iwin, h->isub,
+                                                                             h->iwin_alias ? h->ialias : nullptr,
                                                                              h->F, h->nv, (int)h->fs, win);
       rows(win, h->F, h->nv, h->d_fperm);
       cudaFree(win);
@@ -2116,6 +2196,22 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
   });
 }
 
+// Every captured graph (sweeps, plan, one-graph iteration) and the run_batch
+// twin: dropped whenever a flag changes what a capture records, so the next
+// call re-captures with the new settings on every path (iterate AND
+// run_batch).
+void drop_graphs(tafv_gpu& h) {
+  for (auto& g : h.graphs) {
+    cudaGraphExecDestroy(g.second.exec);
+    for (auto e : g.second.evs) cudaEventDestroy(e);
+  }
+  h.graphs.clear();
+  if (h.plan_graph) cudaGraphExecDestroy(h.plan_graph);
+  h.plan_graph = nullptr;
+  if (h.iter_graph) cudaGraphExecDestroy(h.iter_graph);
+  h.iter_graph = nullptr;
+}
+
 int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
   return guard(h, [&] {
     const std::string n = name ? name : "";
@@ -2123,29 +2219,31 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+      drop_graphs(*h);
     } else if (n == "slot_geo") {
       h->slot_geo = value != 0;
-      for (auto& g : h->graphs) {
-        cudaGraphExecDestroy(g.second.exec);
-        for (auto e : g.second.evs) cudaEventDestroy(e);
+      drop_graphs(*h);
+    } else if (n == "alt_dir") {
+      h->alt_dir = value != 0;
+      drop_graphs(*h);
+    } else if (n == "iwin_alias") {
+      h->iwin_alias = value != 0;
+      // no face is aliased any more: int_window holds every face's window
+      // from here on (K2 accumulates all of them), so stale alias bytes
+      // must not redirect the read-out -- but windows opened while aliased
+      // hold no int_window yet: materialise them first
+      if (!h->iwin_alias && h->ialias) {
+        k_materialise_alias<<<h->grid_for((long long)h->F, 256), 256, 0, h->st>>>(h->iwin, h->isub, h->ialias,
+                                                                                h->F, h->nv, (int)h->fs);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->st));
       }
-      h->graphs.clear();
-    } else if (n == "alt_dir" || n == "iwin_alias") {
-      (n == "alt_dir" ? h->alt_dir : h->iwin_alias) = value != 0;
-      for (auto& g : h->graphs) {
-        cudaGraphExecDestroy(g.second.exec);
-        for (auto e : g.second.evs) cudaEventDestroy(e);
-      }
-      h->graphs.clear();
+      drop_graphs(*h);
     } else if (n == "dl_stream") {
       h->dl_stream = (int)value;
     } else if (n == "face_dx") {
       h->face_dx = value != 0;
-      for (auto& g : h->graphs) {
-        cudaGraphExecDestroy(g.second.exec);
-        for (auto e : g.second.evs) cudaEventDestroy(e);
-      }
-      h->graphs.clear();
+      drop_graphs(*h);
     } else if (n == "batch_lanes") {
       h->batch_lanes = (int)value;
     } else if (n == "plan_graph") {

@@ -18,30 +18,49 @@ def _ptr(a):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def hex_mesh(x, y, z, jitter=0.0, seed=0, permute=False):
-    """Tensor-product hex mesh on node coordinates x[nx+1], y[ny+1], z[nz+1]."""
-    L = N.lib()
-    x = np.ascontiguousarray(x, dtype=np.float64)
-    y = np.ascontiguousarray(y, dtype=np.float64)
-    z = np.ascontiguousarray(z, dtype=np.float64)
-    nx, ny, nz = len(x) - 1, len(y) - 1, len(z) - 1
-    nc, nf = C.c_int32(), C.c_int32()
-    rc = L.tafv_mesh_hex(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), float(jitter), int(seed) & (2**64 - 1),
-                         int(bool(permute)), C.byref(nc), C.byref(nf), *([None] * 9))
-    if rc != 0:
-        raise ValueError("tafv_mesh_hex: invalid spec")
-    nc, nf = nc.value, nf.value
-    m = {
+def _empty_mesh(nc, nf):
+    return {
         "dim": 3,
         "vol": np.empty(nc), "cen": np.empty((nc, 3)), "chl": np.empty(nc),
         "fl": np.empty(nf, dtype=np.int32), "fr": np.empty(nf, dtype=np.int32),
         "fp": np.empty(nf, dtype=np.int32), "fn": np.empty((nf, 3)), "fa": np.empty(nf),
         "fc": np.empty((nf, 3)),
     }
-    rc = L.tafv_mesh_hex(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), float(jitter), int(seed) & (2**64 - 1),
-                         int(bool(permute)), C.byref(C.c_int32()), C.byref(C.c_int32()),
-                         *[_ptr(m[k]) for k in ("vol", "cen", "chl", "fl", "fr", "fp", "fn", "fa", "fc")])
-    if rc != 0:
+
+
+_KEYS = ("vol", "cen", "chl", "fl", "fr", "fp", "fn", "fa", "fc")
+
+
+def hex_mesh(x, y, z, jitter=0.0, seed=0, permute=False, window=None, lib=None):
+    """Tensor-product hex mesh on node coordinates x[nx+1], y[ny+1], z[nz+1].
+
+    window = (i0, i1, j0, j1, k0, k1): only those cells of the same lattice
+    (tafv_mesh_hex_window), bitwise the full mesh's cells there. `lib` is
+    any ctypes library exporting the generator (default: the product
+    library; the oracle's checker library compiles the same generator)."""
+    L = lib if lib is not None else N.lib()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    nx, ny, nz = len(x) - 1, len(y) - 1, len(z) - 1
+    sd = int(seed) & (2**64 - 1)
+    if window is None:
+        def call(nc, nf, arrs):
+            return L.tafv_mesh_hex(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), float(jitter), sd,
+                                   int(bool(permute)), nc, nf, *arrs)
+    else:
+        if permute:
+            raise ValueError("hex_mesh: a window of a permuted mesh is not defined")
+        box = np.ascontiguousarray(window, dtype=np.int32)
+
+        def call(nc, nf, arrs):
+            return L.tafv_mesh_hex_window(nx, ny, nz, _ptr(x), _ptr(y), _ptr(z), _ptr(box), float(jitter),
+                                          sd, nc, nf, *arrs)
+    nc, nf = C.c_int32(), C.c_int32()
+    if call(C.byref(nc), C.byref(nf), [None] * 9) != 0:
+        raise ValueError("tafv_mesh_hex: invalid spec")
+    m = _empty_mesh(nc.value, nf.value)
+    if call(C.byref(C.c_int32()), C.byref(C.c_int32()), [_ptr(m[k]) for k in _KEYS]) != 0:
         raise ValueError("tafv_mesh_hex: invalid spec")
     return m
 

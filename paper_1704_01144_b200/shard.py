@@ -98,3 +98,38 @@ def level_cost_weights(tau, theta=None):
     tau = _np.asarray(tau)
     th = int(tau.max()) if theta is None else int(theta)
     return _np.ldexp(1.0, th - tau)
+
+
+def smooth_levels(mesh, tau):
+    """smooth_to_fixpoint (levels.cpp:33-51) on the host (tafv_level_smooth)."""
+    lib = N.lib()
+    mv, keep = mesh_view(mesh)
+    t = np.ascontiguousarray(tau, dtype=np.int32).copy()
+    if lib.tafv_level_smooth(C.byref(mv), _ptr(t)) != 0:
+        raise ValueError(lib.tafv_shard_last_error().decode())
+    return t
+
+
+def initial_levels(mesh, w, opt, gamma=1.4):
+    """The levels plan_iteration would assign to the Euler state w (host,
+    for slab cut weights only -- not bit-exact: the device plan is the
+    authority): dt_max = cfl h / (|u| + c) (kernels.cpp:247-254), raw =
+    ilogb(dt_max / dt_min) clamped to [0, theta_max] (levels.cpp:18-25),
+    smoothed to the fixpoint."""
+    w = np.asarray(w, dtype=np.float64).reshape(len(mesh["vol"]), -1)
+    rho = w[:, 0]
+    u = w[:, 1:4] / rho[:, None]
+    p = (gamma - 1.0) * (w[:, 4] - 0.5 * rho * (u * u).sum(axis=1))
+    speed = np.sqrt((u * u).sum(axis=1)) + np.sqrt(gamma * np.maximum(p, 0.0) / rho)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        dtm = np.where(speed > 0, np.minimum(opt.dt_cap, opt.cfl * mesh["chl"] / speed), opt.dt_cap)
+    ratio = dtm / dtm.min()
+    raw = np.frexp(ratio)[1] - 1  # ilogb for ratio >= 1
+    raw = np.clip(np.where(ratio >= 1.0, raw, 0), 0, opt.theta_max).astype(np.int32)
+    return smooth_levels(mesh, raw)
+
+
+def initial_level_cost(mesh, w, opt):
+    """Per-cell level cost 2^(theta - tau) of the initial plan: the weights
+    of the slab cut (DistDriver::repartition, exchange.cpp:598-603)."""
+    return level_cost_weights(initial_levels(mesh, w, opt))

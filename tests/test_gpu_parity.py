@@ -713,3 +713,87 @@ def test_raw_levels_and_dt_max_arrays(gpu):
     tau = g.get_array("tau")
     g.inject_levels(np.zeros_like(tau), 1e-6, opt)
     assert (g.get_array("raw_level") == raw).all()
+
+
+def test_run_batch_rejects_unsafe_buffers(gpu):
+    """run_batch copies rows*nv*8 bytes through raw pointers: float32,
+    non-contiguous, device-resident or read-only buffers are refused before
+    any copy."""
+    import torch
+    cfg = configs.get(2, 8)
+    mesh = cfg.mesh()
+    s = Solver(mesh, "euler")
+    W0 = np.ascontiguousarray(cfg.initial_state(mesh) * mesh["vol"][:, None])
+    good = np.empty_like(W0)
+    bad_inputs = [W0.astype(np.float32), np.asfortranarray(W0), W0.reshape(-1)[::1].reshape(W0.shape).T,
+                  torch.from_numpy(W0).cuda()]
+    for bad in bad_inputs:
+        with pytest.raises(InvalidArgument):
+            s.run_batch([bad], [good], cfg.options(), 1)
+    ro = np.empty_like(W0)
+    ro.flags.writeable = False
+    with pytest.raises(InvalidArgument):
+        s.run_batch([W0], [ro], cfg.options(), 1)
+    s.run_batch([W0], [good], cfg.options(), 1)  # still usable afterwards
+
+
+def test_iwin_alias_switch_off_mid_session(gpu):
+    """Switching the equal-level int_window alias off after aliased
+    iterations materialises the aliased windows: int_window reads and the
+    following iterations are bitwise those of a handle run unaliased from
+    the start, through iterate and through run_batch (whose one-graph
+    iteration is re-captured)."""
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    a, b = Solver(mesh, "euler"), Solver(mesh, "euler")
+    b.set_flag("iwin_alias", 0)
+    for s in (a, b):
+        s.set_state(w0)
+        s.reference_integrate(cfg.options(), 2)
+    a.set_flag("iwin_alias", 0)
+    assert a.get_array("int_window").tobytes() == b.get_array("int_window").tobytes()
+    for s in (a, b):
+        s.reference_integrate(cfg.options(), 2)
+    assert a.get_array("int_window").tobytes() == b.get_array("int_window").tobytes()
+    assert a.get_state()[1].tobytes() == b.get_state()[1].tobytes()
+    W = np.ascontiguousarray(a.get_state()[1])
+    oa, ob = np.empty_like(W), np.empty_like(W)
+    a.set_flag("iwin_alias", 1)
+    a.run_batch([W], [oa], cfg.options(), 2)
+    a.set_flag("iwin_alias", 0)
+    a.run_batch([W], [oa], cfg.options(), 2)
+    b.run_batch([W], [ob], cfg.options(), 2)
+    assert oa.tobytes() == ob.tobytes()
+    assert a.get_array("int_window").tobytes() == b.get_array("int_window").tobytes()
+
+
+def test_iterate_host_equals_device_resident(gpu):
+    """tafv_gpu_iterate_host (state in the caller's host buffer, W up and
+    down every iteration, chunked duplex copies) is bitwise
+    set_state(None, W) + reference_integrate: the same W after every
+    iteration and the same records; a small chunk count and a large one."""
+    cfg = configs.get(2, 6)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    a = Solver(mesh, "euler")
+    a.set_state(w0)
+    a.reference_integrate(cfg.options(), 1)
+    W = np.ascontiguousarray(a.get_state()[1])
+    ra = a.reference_integrate(cfg.options(), 3)
+    b = Solver(mesh, "euler")
+    b.set_state(None, W, ra[0]["t_start"], 1)
+    Wh = W.copy()
+    rb = b.iterate_host(Wh, cfg.options(), 3)
+    assert Wh.tobytes() == a.get_state()[1].tobytes()
+    assert b.get_state()[1].tobytes() == Wh.tobytes()
+    for x, y in zip(ra, rb):
+        assert x == y
+    import torch
+    Wt = torch.from_numpy(W.copy()).pin_memory()
+    c = Solver(mesh, "euler")
+    c.set_state(None, W, ra[0]["t_start"], 1)
+    c.iterate_host(Wt, cfg.options(), 3)
+    assert Wt.numpy().tobytes() == Wh.tobytes()
+    with pytest.raises(InvalidArgument):
+        c.iterate_host(W.astype(np.float32), cfg.options(), 1)
