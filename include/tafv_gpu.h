@@ -80,7 +80,13 @@ typedef struct tafv_options {
   double dt_cap;
 } tafv_options;
 
-/* IterationRecord (reference.hpp:20-29); total_extensive per component. */
+/* IterationRecord (reference.hpp:20-29); total_extensive per component.
+ * boundary_flux (new, the conservation ledger): per component, what the
+ * iteration's correctors took out of the domain through transmissive
+ * boundary faces (the sum of those faces' int_substep integrals, each the
+ * +sign*phi term of its left cell's flux_sum_correct, kernels.cpp:204-216),
+ * so that total_extensive(n) = total_extensive(n-1) - boundary_flux(n) up to
+ * rounding. Compensated sums; 0 on closed / periodic meshes. */
 typedef struct tafv_record {
   int32_t iteration;
   int32_t theta;
@@ -92,6 +98,7 @@ typedef struct tafv_record {
   int64_t level_cells[TAFV_MAX_LEVELS];
   int32_t n_levels;
   int32_t nv;
+  double boundary_flux[8];
 } tafv_record;
 
 /* Summary of an IterationPlan (levels.hpp:46-61) held on the device.

@@ -39,6 +39,7 @@ struct IterationRecord {  // reference.hpp:20-29
   double advance = 0.0;
   std::vector<double> total_extensive;  // one sum per conserved component
   double cost_ratio = 1.0;
+  std::vector<double> boundary_flux;    // new: outflow through transmissive faces (ledger)
   std::vector<int64_t> level_cells;
 };
 
@@ -59,6 +60,7 @@ inline IterationRecord to_record(const tafv_record& r) {
   o.theta = r.theta;
   o.advance = r.advance;
   o.total_extensive.assign(r.total_extensive, r.total_extensive + r.nv);
+  o.boundary_flux.assign(r.boundary_flux, r.boundary_flux + r.nv);
   o.cost_ratio = r.cost_ratio;
   o.level_cells.assign(r.level_cells, r.level_cells + r.n_levels);
   return o;

@@ -67,6 +67,7 @@ struct Record {  // layout mirrors tafv_record in include/tafv_gpu.h
   int64_t level_cells[16];
   int32_t n_levels;
   int32_t nv;
+  double boundary_flux[8];  // not kept by the reference: zero
 };
 
 void fill(Record* out, const IterationRecord& r) {

@@ -484,6 +484,7 @@ struct Record {  // mirrors tafv_record (include/tafv_gpu.h)
   int64_t level_cells[16];
   int32_t n_levels;
   int32_t nv;
+  double boundary_flux[8];  // ledger (new): outflow through transmissive faces this iteration
 };
 
 template <class P>
@@ -826,6 +827,7 @@ struct Driver {
     k.limit_gradients(cells.data(), nc, front, kCorrector);
     k.reconstruct_faces(faces.data(), nf, front, kCorrector);
     k.riemann_correct(plan.face_cadence, dt, faces.data(), nf, front);
+    ledger(faces.data(), nf);
     k.flux_sum_correct(tau, plan.face_cadence, cells.data(), nc, front);
     k.extensive_correct(cells.data(), nc);
     k.intensive_correct(tau, cells.data(), nc, front);
@@ -847,6 +849,26 @@ struct Driver {
     k.intensive_predict(cells.data(), nc);
   }
 
+  // Conservation ledger (new; the reference keeps none): a transmissive
+  // face's slot adds +int_substep to its left cell's residual sum
+  // (flux_sum_correct, kernels.cpp:204-216: tau_c == cadence_f on a boundary
+  // face, so the substep integral is the one read), i.e. takes it out of the
+  // domain. Summed over the active boundary faces of every corrector, in
+  // ascending face id, compensated (TwoSum).
+  double bflux[8] = {}, bcomp[8] = {};
+  void ledger(const int* faces, int64_t nf) {
+    for (int64_t i = 0; i < nf; ++i) {
+      const int f = faces[i];
+      if (m.resolved_right(f) >= 0) continue;
+      for (int k = 0; k < P::NV; ++k) {
+        const double b = st.int_substep[f * P::NV + k];
+        const double s = bflux[k] + b, bb = s - bflux[k];
+        bcomp[k] += (bflux[k] - (s - bb)) + (b - bb);
+        bflux[k] = s;
+      }
+    }
+  }
+
   void totals(double* out) const {  // state.cpp:40-44 (ascending id, per component)
     for (int j = 0; j < P::NV; ++j) {
       double total = 0.0;
@@ -864,6 +886,7 @@ struct Driver {
     r.theta = plan.theta();
     r.advance = plan.levels.dt * static_cast<double>(plan.subiterations());
     totals(r.total_extensive);
+    for (int k = 0; k < P::NV; ++k) r.boundary_flux[k] = bflux[k] + bcomp[k];
     r.cost_ratio = plan.levels.cost_ratio();
     r.n_levels = static_cast<int32_t>(plan.levels.cells_of_level.size());
     for (int l = 0; l < r.n_levels && l < 16; ++l)
@@ -892,6 +915,7 @@ struct Driver {
     const double t_start = st.t0;
     const Items none;
     reset_fronts(st);
+    for (int k = 0; k < 8; ++k) bflux[k] = bcomp[k] = 0.0;
     const int subiterations = plan.subiterations();
     for (int s = 1; s <= subiterations; ++s) {
       const int level = subiteration_level(s, theta);
@@ -933,7 +957,9 @@ struct Driver {
       k.green_gauss_gradient(cells.data(), nc, 1, kCorrector);
       k.limit_gradients(cells.data(), nc, 1, kCorrector);
       k.reconstruct_faces(faces.data(), nf, 1, kCorrector);
+      for (int q = 0; q < 8; ++q) bflux[q] = bcomp[q] = 0.0;
       k.riemann_correct(cad, dt, faces.data(), nf, 1);
+      ledger(faces.data(), nf);
       k.flux_sum_correct(tau, cad, cells.data(), nc, 1);
       k.extensive_correct(cells.data(), nc);
       k.intensive_correct(tau, cells.data(), nc, 1);
@@ -948,6 +974,7 @@ struct Driver {
       r.theta = 0;
       r.advance = dt;
       totals(r.total_extensive);
+      for (int q = 0; q < P::NV; ++q) r.boundary_flux[q] = bflux[q] + bcomp[q];
       r.cost_ratio = 1.0;
       r.n_levels = 1;
       r.level_cells[0] = m.nc;

@@ -55,6 +55,7 @@ class Record(C.Structure):
         ("level_cells", C.c_int64 * MAX_LEVELS),
         ("n_levels", C.c_int32),
         ("nv", C.c_int32),
+        ("boundary_flux", C.c_double * 8),
     ]
 
     def as_dict(self):
@@ -67,6 +68,7 @@ class Record(C.Structure):
             "cost_ratio": self.cost_ratio,
             "total_extensive": list(self.total_extensive[: self.nv]),
             "level_cells": list(self.level_cells[: self.n_levels]),
+            "boundary_flux": list(self.boundary_flux[: self.nv]),
         }
 
 

@@ -48,7 +48,10 @@ struct MeshDev {
   const int* __restrict__ adj_off;  // [N+1]
   const int* __restrict__ adj_face; // [M] face id (~f when the cell is the face's right side)
   const int* __restrict__ adj_nb;   // [M] neighbour cell (-1 across transmissive faces)
-  const int2* __restrict__ lr;      // [F] {left, resolved right (-1 transmissive)}
+  // [F] {left, resolved right}; a transmissive boundary face (no right
+  // cell) carries -2 - b, b its index among the boundary faces (the
+  // ledger row of StateDev::bsum): every "right >= 0" test is unchanged.
+  const int2* __restrict__ lr;
   const int* __restrict__ rcf;      // [F] face whose centroid the right side uses (periodic), or null
   const double4* __restrict__ geo;  // [F] {nx, ny, nz, area}
   const double* __restrict__ fcen;  // [F][3]
@@ -82,6 +85,12 @@ struct StateDev {
   // `ialias` set K2 skips those faces' window reset and accumulation and
   // records alias = 1; get_array("int_window") materialises isub + 0.0.
   uint8_t* ialias;
+  // [NB][NV] or null: conservation ledger -- per transmissive boundary face
+  // the sum of the int_substep integrals its left cell's correctors took
+  // out of the domain (flux_sum_correct, kernels.cpp:204-216: a boundary
+  // slot contributes +int_substep to the residual's sum) since the last
+  // trailing corrector, which reduces and clears them (k_totals).
+  double* bsum;
 };
 
 struct PlanDev {
@@ -92,6 +101,7 @@ struct PlanDev {
   long long face_count[kMaxLevels];
   long long fringe_count[kMaxLevels];
   double totals[8];     // sum of W per component after the last iteration
+  double bflux[8];      // boundary outflow per component over the last iteration (ledger)
   int ncell_prefix[kMaxLevels];  // |{c owned : tau_c <= l}|: K3 active cells of level l
   int nface_prefix[kMaxLevels];  // |{f touching owned : cadence_f <= l}|: K2 active faces
   // K1 active cells. Single domain: the K3 list. Shards: two lists, so the
@@ -400,6 +410,18 @@ __device__ __forceinline__ void load_grad(const StateDev& s, int x, double* g) {
   }
 }
 
+#ifndef TAFV_LEDGER
+#define TAFV_LEDGER 1
+#endif
+// Ledger: the int_substep row this thread just stored, added to its
+// boundary face's running outflow (re-read from L1/L2 instead of kept live
+// across the store: K2 is register-bound).
+template <int NV>
+__device__ __forceinline__ void ledger_add(double* bs, const double* isub) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) bs[k] = bs[k] + __ldcg(isub + k);
+}
+
 // ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
 #ifndef TAFV_K2_MINB
 #define TAFV_K2_MINB 7
@@ -515,6 +537,9 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
 #pragma unroll
       for (int q = 0; q < FS; q += 2) st2(isub + q, row[q], row[q + 1]);
       if (s.ialias) s.ialias[f] = skip ? 1 : 0;
+#if TAFV_LEDGER
+      if (lr.y < -1 && s.bsum) ledger_add<NV>(s.bsum + (size_t)(-2 - lr.y) * NV, isub);
+#endif
     }
   }
 }
@@ -622,8 +647,12 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
 }
 
 // Fixed-order reduction of the per-block partials: block k reduces
-// component k (deterministic tree over a fixed number of partials).
-__global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan) {
+// component k (deterministic tree over a fixed number of partials). The same
+// block reduces the ledger's per-face boundary outflows of component k
+// (compensated, fixed shape) into plan->bflux[k] and clears them for the
+// next iteration.
+__global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan, double* bsum,
+                                                int nb, int nv) {
   __shared__ DD red[256];
   const int k = blockIdx.x;
   DD a{0.0, 0.0};
@@ -635,6 +664,21 @@ __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks,
     __syncthreads();
   }
   if (threadIdx.x == 0) plan->totals[k] = red[0].hi + red[0].lo;
+  __syncthreads();
+  DD o{0.0, 0.0};
+  if (bsum)
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      double* p = bsum + (size_t)b * nv + k;
+      o = dd_add(o, *p);
+      *p = 0.0;
+    }
+  red[threadIdx.x] = o;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) plan->bflux[k] = red[0].hi + red[0].lo;
 }
 
 // ---- plan kernels ----------------------------------------------------------

@@ -166,6 +166,8 @@ struct tafv_gpu {
   size_t fs = 0;  // face-integral row stride in doubles (padded, see FaceRow)
   double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
   uint8_t* ialias = nullptr;  // [F] see StateDev::ialias
+  int NB = 0;                 // transmissive boundary faces (MeshDev::lr)
+  double* bsum = nullptr;     // [NB][nv] see StateDev::bsum
   bool iwin_alias = true;
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
   uint8_t* fflag = nullptr;
@@ -263,7 +265,7 @@ struct tafv_gpu {
                    slot_geo ? sdx : nullptr, face_dx ? fdx : nullptr};
   }
   StateDev state_dev() const {
-    return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr};
+    return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr, bsum};
   }
 
   double* staging(size_t n) {
@@ -297,7 +299,7 @@ struct tafv_gpu {
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
-    void* ptrs[] = {w,     W,        wp,
+    void* ptrs[] = {w,     W,        wp,       bsum,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
@@ -613,13 +615,14 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
     for (int d = 0; d < 3; ++d) cen[3 * (size_t)i + d] = mv.cell_centroid[3 * (size_t)c + d];
   }
   std::vector<int2> lr(F);
+  h.NB = 0;
   std::vector<int> rcf(h.periodic ? F : 0);
   std::vector<double4> geo(F);
   std::vector<double> fcen(3 * (size_t)F);
   for (int j = 0; j < F; ++j) {
     const int f = h.fperm[j];
     const int rr = resolved_right(f);
-    lr[j] = make_int2(cinv[mv.face_left[f]], rr >= 0 ? cinv[rr] : -1);
+    lr[j] = make_int2(cinv[mv.face_left[f]], rr >= 0 ? cinv[rr] : -2 - h.NB++);
     if (h.periodic) rcf[j] = (mv.face_right[f] < 0 && mv.face_partner[f] >= 0) ? finv[mv.face_partner[f]] : j;
     geo[j] = make_double4(mv.face_normal[3 * (size_t)f], mv.face_normal[3 * (size_t)f + 1],
                           mv.face_normal[3 * (size_t)f + 2], mv.face_area[f]);
@@ -728,6 +731,8 @@ void alloc_state(tafv_gpu& h) {
   CK(cudaMemset(h.iwin, 0, F * h.fs * sizeof(double)));
   h.ialias = dalloc<uint8_t>(F);
   CK(cudaMemset(h.ialias, 0, F));
+  h.bsum = dalloc<double>(std::max<size_t>(1, (size_t)h.NB * nv));
+  CK(cudaMemset(h.bsum, 0, std::max<size_t>(1, (size_t)h.NB * nv) * sizeof(double)));
   h.tau = dalloc<int8_t>(N);
   h.raw = dalloc<int8_t>(N);
   h.tmpa = dalloc<int8_t>(N);
@@ -1265,10 +1270,11 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
       k_gather_update<P, false, true, DEG><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, ncp,
                                                                           h.dplan, h.partials, 0);
     }, na, nf, 0);
-    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan);
+    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, h.bsum, h.NB, P::NV);
     h.launches += 4;
     if (h.sharded()) {
       h.comm->allreduce_sum_f64(h.rank, h.dplan->totals, P::NV, h.st);
+      h.comm->allreduce_sum_f64(h.rank, h.dplan->bflux, P::NV, h.st);
       h.comm->allreduce_max_i32(h.rank, &h.dplan->nonfinite, 1, h.st);
     }
     halo_rows(h, h.w, P::NV, true);  // the next iteration stages the halo's new w
@@ -1373,6 +1379,7 @@ void close_iteration(tafv_gpu& h, tafv_record* rec) {
     rec->cost_ratio = pi.cost_ratio;
     rec->nv = h.nv;
     for (int k = 0; k < h.nv; ++k) rec->total_extensive[k] = h.hplan->totals[k];
+    for (int k = 0; k < h.nv; ++k) rec->boundary_flux[k] = h.hplan->bflux[k];
     rec->n_levels = h.theta + 1;
     for (int l = 0; l <= h.theta; ++l) rec->level_cells[l] = h.gcount[l];
   }
@@ -1908,6 +1915,7 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->n_k1 = h.n_k1;
     t->F_own = h.F_own;
     t->N_global = h.N_global;
+    t->NB = h.NB;
     alloc_state(*t);
     set_grids(*t);
   } catch (...) {

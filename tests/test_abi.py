@@ -28,12 +28,30 @@ def test_library_exports_every_declared_symbol():
     assert sorted(N.EXPORTS) == declared
 
 
-def test_struct_layouts_match_header():
-    # sizes of the ABI structs as laid out by the C compiler (x86-64 SysV)
-    assert C.sizeof(N.MeshView) == 4 * 3 + 4 + 9 * 8
-    assert C.sizeof(N.Record) == 8 + 4 * 8 + 8 * 8 + 16 * 8 + 8
-    assert C.sizeof(N.Options) == 24
-    assert C.sizeof(N.PlanInfo) == 8 + 16 + 3 * 16 * 8 + 3 * 8
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors have the C compiler's layout of the header's
+    structs: sizeof and every field offset (gcc on include/tafv_gpu.h)."""
+    import subprocess
+    structs = {"tafv_mesh_view": N.MeshView, "tafv_record": N.Record, "tafv_options": N.Options,
+               "tafv_plan_info": N.PlanInfo, "tafv_physics": N.Physics}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tafv_gpu.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {(a, b): int(c) for a, b, c in (l.split() for l in out if l.strip())}
+    for cname, py in structs.items():
+        assert got[(cname, "sizeof")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
+    import oracle
+    assert C.sizeof(oracle.Record) == C.sizeof(N.Record)
 
 
 def test_create_without_gpu_fails_loudly_or_succeeds():
