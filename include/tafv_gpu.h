@@ -200,7 +200,9 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
 
 /* Debug/parity access to intermediate SolverState arrays in original ids:
  * "w_pred" [nc][nv], "grad" [nc][nv][3], "phi_pred" / "int_substep" /
- * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32). */
+ * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32);
+ * "mesh_digest" [20] (uint64: FNV-1a of every internal mesh array, slot
+ * count, boundary count, flags -- compares the device and host builds). */
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
 
 /* Launch configuration knobs (bench/profiling):

@@ -263,6 +263,8 @@ class Solver:
     def get_array(self, name):
         if name in ("raw_level", "tau"):
             out = np.zeros(self.nc, dtype=np.int32)
+        elif name == "mesh_digest":
+            out = np.zeros(20, dtype=np.uint64)
         else:
             rows = self.nf if name in ("phi_pred", "int_substep", "int_window") else self.nc
             width = {"grad": self.nv * 3, "dt_max": 1}.get(name, self.nv)

@@ -48,10 +48,7 @@ struct MeshDev {
   const int* __restrict__ adj_off;  // [N+1]
   const int* __restrict__ adj_face; // [M] face id (~f when the cell is the face's right side)
   const int* __restrict__ adj_nb;   // [M] neighbour cell (-1 across transmissive faces)
-  // [F] {left, resolved right}; a transmissive boundary face (no right
-  // cell) carries -2 - b, b its index among the boundary faces (the
-  // ledger row of StateDev::bsum): every "right >= 0" test is unchanged.
-  const int2* __restrict__ lr;
+  const int2* __restrict__ lr;      // [F] {left, resolved right (-1 transmissive)}
   const int* __restrict__ rcf;      // [F] face whose centroid the right side uses (periodic), or null
   const double4* __restrict__ geo;  // [F] {nx, ny, nz, area}
   const double* __restrict__ fcen;  // [F][3]
@@ -85,12 +82,6 @@ struct StateDev {
   // `ialias` set K2 skips those faces' window reset and accumulation and
   // records alias = 1; get_array("int_window") materialises isub + 0.0.
   uint8_t* ialias;
-  // [NB][NV] or null: conservation ledger -- per transmissive boundary face
-  // the sum of the int_substep integrals its left cell's correctors took
-  // out of the domain (flux_sum_correct, kernels.cpp:204-216: a boundary
-  // slot contributes +int_substep to the residual's sum) since the last
-  // trailing corrector, which reduces and clears them (k_totals).
-  double* bsum;
 };
 
 struct PlanDev {
@@ -410,18 +401,6 @@ __device__ __forceinline__ void load_grad(const StateDev& s, int x, double* g) {
   }
 }
 
-#ifndef TAFV_LEDGER
-#define TAFV_LEDGER 1
-#endif
-// Ledger: the int_substep row this thread just stored, added to its
-// boundary face's running outflow (re-read from L1/L2 instead of kept live
-// across the store: K2 is register-bound).
-template <int NV>
-__device__ __forceinline__ void ledger_add(double* bs, const double* isub) {
-#pragma unroll
-  for (int k = 0; k < NV; ++k) bs[k] = bs[k] + __ldcg(isub + k);
-}
-
 // ---- K2: window reset + reconstruction + Rusanov + predict/correct ---------
 #ifndef TAFV_K2_MINB
 #define TAFV_K2_MINB 7
@@ -537,9 +516,6 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
 #pragma unroll
       for (int q = 0; q < FS; q += 2) st2(isub + q, row[q], row[q + 1]);
       if (s.ialias) s.ialias[f] = skip ? 1 : 0;
-#if TAFV_LEDGER
-      if (lr.y < -1 && s.bsum) ledger_add<NV>(s.bsum + (size_t)(-2 - lr.y) * NV, isub);
-#endif
     }
   }
 }
@@ -643,6 +619,27 @@ __global__ void __launch_bounds__(128) k_gather_update(MeshDev m, StateDev s,
       for (int q = 1; q < (int)(blockDim.x >> 5); ++q) b = dd_merge(b, wred[q][threadIdx.x]);
       partials[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = b;
     }
+  }
+}
+
+// Conservation ledger (new; the reference keeps none). A transmissive
+// face's slot adds +int_substep to its left cell's residual sum
+// (flux_sum_correct, kernels.cpp:204-216: tau_c == cadence_f on a boundary
+// face, so the substep integral is the one read), i.e. takes it out of the
+// domain. After each corrector's K2, on a side stream (off the critical
+// path), every boundary face active at `level` (cadence <= level) adds its
+// int_substep row to its running outflow bsum[b]; the trailing corrector's
+// k_totals reduces and clears them. bface[b] = internal id of the b-th
+// transmissive face touching an owned cell.
+template <int NV>
+__global__ void __launch_bounds__(256) k_ledger(const int* __restrict__ bface, int nb,
+                                                const int8_t* __restrict__ cad, int level,
+                                                const double* __restrict__ isub, int fs, double* bsum) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const int j = bface[b];
+    if (cad[j] > level) continue;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bsum[(size_t)b * NV + k] += isub[(size_t)j * fs + k];
   }
 }
 

@@ -40,8 +40,11 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "comm.h"
 #include "kernels.cuh"
+#include "meshprep.cuh"
 #include "shard.h"
 #include "tafv_gpu.h"
 
@@ -166,8 +169,13 @@ struct tafv_gpu {
   size_t fs = 0;  // face-integral row stride in doubles (padded, see FaceRow)
   double *phi = nullptr, *isub = nullptr, *iwin = nullptr;
   uint8_t* ialias = nullptr;  // [F] see StateDev::ialias
-  int NB = 0;                 // transmissive boundary faces (MeshDev::lr)
-  double* bsum = nullptr;     // [NB][nv] see StateDev::bsum
+  // conservation ledger (k_ledger): transmissive faces touching owned cells
+  int NB = 0;
+  int* bface = nullptr;       // [NB] internal face ids (mesh, shared with the twin)
+  double* bsum = nullptr;     // [NB][nv] running outflow since the last trailing corrector
+  cudaStream_t lst = nullptr; // side stream of the ledger kernels
+  cudaEvent_t ev_led_fork = nullptr, ev_led = nullptr;
+  bool led_pending = false;
   bool iwin_alias = true;
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
   uint8_t* fflag = nullptr;
@@ -265,7 +273,7 @@ struct tafv_gpu {
                    slot_geo ? sdx : nullptr, face_dx ? fdx : nullptr};
   }
   StateDev state_dev() const {
-    return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr, bsum};
+    return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr};
   }
 
   double* staging(size_t n) {
@@ -295,7 +303,7 @@ struct tafv_gpu {
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     if (owns_mesh) {
       void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
-                           d_cperm, d_fperm, fint};
+                           d_cperm, d_fperm, fint, bface};
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
@@ -321,6 +329,9 @@ struct tafv_gpu {
     for (auto& e : ev_chunk) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
     if (cst) cudaStreamDestroy(cst);
+    if (lst) cudaStreamDestroy(lst);
+    if (ev_led_fork) cudaEventDestroy(ev_led_fork);
+    if (ev_led) cudaEventDestroy(ev_led);
     if (ev_pack) cudaEventDestroy(ev_pack);
     if (ev_halo) cudaEventDestroy(ev_halo);
   }
@@ -475,8 +486,8 @@ namespace {
 // ---- mesh upload -----------------------------------------------------------
 // cls (optional): per original cell 0 owned / 1 ring 1 / 2 ring 2 (shards);
 // touch (optional): per original face 1 if it has an owned side.
-void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
-                 const uint8_t* touch = nullptr) {
+void upload_mesh_host(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
+                      const uint8_t* touch = nullptr) {
   const int N = mv.n_cells, F = mv.n_faces;
   require(N > 0 && F >= 0, "mesh: empty mesh");
   require(mv.dim >= 1 && mv.dim <= 3, "mesh: dim must be 1, 2 or 3");
@@ -615,14 +626,15 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
     for (int d = 0; d < 3; ++d) cen[3 * (size_t)i + d] = mv.cell_centroid[3 * (size_t)c + d];
   }
   std::vector<int2> lr(F);
-  h.NB = 0;
+  std::vector<int> bface;  // ledger: transmissive faces touching owned cells
   std::vector<int> rcf(h.periodic ? F : 0);
   std::vector<double4> geo(F);
   std::vector<double> fcen(3 * (size_t)F);
   for (int j = 0; j < F; ++j) {
     const int f = h.fperm[j];
     const int rr = resolved_right(f);
-    lr[j] = make_int2(cinv[mv.face_left[f]], rr >= 0 ? cinv[rr] : -2 - h.NB++);
+    lr[j] = make_int2(cinv[mv.face_left[f]], rr >= 0 ? cinv[rr] : -1);
+    if (rr < 0 && j < h.F_own) bface.push_back(j);
     if (h.periodic) rcf[j] = (mv.face_right[f] < 0 && mv.face_partner[f] >= 0) ? finv[mv.face_partner[f]] : j;
     geo[j] = make_double4(mv.face_normal[3 * (size_t)f], mv.face_normal[3 * (size_t)f + 1],
                           mv.face_normal[3 * (size_t)f + 2], mv.face_area[f]);
@@ -709,6 +721,249 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
   up(h.d_cperm, h.cperm);
   h.d_fperm = dalloc<int>(F);
   up(h.d_fperm, h.fperm);
+  h.NB = (int)bface.size();
+  h.bface = dalloc<int>(std::max(1, h.NB));
+  if (h.NB) up(h.bface, bface);
+}
+
+// Device build of the same arrays (meshprep.cuh): the raw mesh goes up once
+// and the orderings, CSR, closure check and derived geometry are computed on
+// the GPU -- seconds instead of minutes at 80M cells, and no host copies of
+// the 32-byte-per-slot streams. Bitwise the host build's arrays
+// (test_device_mesh_build_equals_host_build).
+void upload_mesh_device(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
+                        const uint8_t* touch = nullptr) {
+  using namespace tafv::prep;
+  const int N = mv.n_cells, F = mv.n_faces;
+  require(N > 0 && F >= 0, "mesh: empty mesh");
+  require(mv.dim >= 1 && mv.dim <= 3, "mesh: dim must be 1, 2 or 3");
+  h.N = N;
+  h.F = F;
+  h.dim = mv.dim;
+  cudaStream_t st = h.st;
+  std::vector<void*> tmp;  // temporaries, freed on every exit path
+  struct Guard {
+    std::vector<void*>& t;
+    ~Guard() {
+      for (void* p : t) cudaFree(p);
+    }
+  } guard{tmp};
+  auto talloc = [&](size_t bytes) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+    tmp.push_back(p);
+    return p;
+  };
+  auto tfree = [&](void* p) {
+    auto it = std::find(tmp.begin(), tmp.end(), p);
+    if (it != tmp.end()) {
+      cudaFree(p);
+      tmp.erase(it);
+    }
+  };
+  auto up = [&](const void* src, size_t bytes) {
+    void* d = talloc(bytes);
+    CK(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st));
+    return d;
+  };
+  const int G = h.sms * 8, B = 256;
+  int* flags = (int*)talloc(sizeof(int));
+  CK(cudaMemsetAsync(flags, 0, sizeof(int), st));
+  const int* fl = (const int*)up(mv.face_left, (size_t)F * 4);
+  const int* fr = (const int*)up(mv.face_right, (size_t)F * 4);
+  const int* fp = (const int*)up(mv.face_partner, (size_t)F * 4);
+  k_check_faces<<<G, B, 0, st>>>(fl, fr, fp, N, F, flags);
+  int hflags = 0;
+  CK(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  require(!(hflags & 1), "mesh: face left cell out of range");
+  require(!(hflags & 2), "mesh: face right cell out of range");
+  require(!(hflags & 4), "mesh: periodic partner out of range");
+  h.periodic = (hflags & 8) != 0;
+  const double* cen0 = (const double*)up(mv.cell_centroid, (size_t)N * 24);
+  const double* vol0 = (const double*)up(mv.cell_volume, (size_t)N * 8);
+  const double* chl0 = (const double*)up(mv.cell_char_length, (size_t)N * 8);
+
+  // cell order: (class, Morton, id) -- the class pass only on shards
+  std::vector<uint8_t> cls4;
+  if (cls) {
+    cls4.resize(N);
+    for (int c = 0; c < N; ++c) cls4[c] = cls[c] == 0 ? 0 : (uint8_t)(cls[c] + 1);
+    for (int f = 0; f < F; ++f) {
+      const int l = mv.face_left[f];
+      const int r = mv.face_right[f] >= 0 ? mv.face_right[f]
+                    : mv.face_partner[f] >= 0 ? mv.face_left[mv.face_partner[f]] : -1;
+      if (r < 0) continue;
+      if (cls[l] == 0 && cls[r] != 0) cls4[l] = 1;
+      if (cls[r] == 0 && cls[l] != 0) cls4[r] = 1;
+    }
+  }
+  h.n_deep = h.n_own = h.n_k1 = 0;
+  for (int c = 0; c < N; ++c) {
+    const int k = cls ? cls4[c] : 0;
+    if (k == 0) ++h.n_deep;
+    if (k <= 1) ++h.n_own;
+    if (k <= 2) ++h.n_k1;
+  }
+  double* part = (double*)talloc((size_t)G * 6 * 8);
+  double* box = (double*)talloc(6 * 8);
+  k_bbox_partial<<<G, 256, 0, st>>>(cen0, N, part);
+  k_bbox_final<<<1, 32, 0, st>>>(part, G, box);
+  size_t need = 0, have = 0;
+  void* sort_tmp = nullptr;
+  auto scratch = [&](size_t bytes) {
+    if (bytes > have) {
+      if (sort_tmp) tfree(sort_tmp);
+      sort_tmp = talloc(bytes);
+      have = bytes;
+    }
+    return sort_tmp;
+  };
+  h.d_cperm = dalloc<int>(N);
+  {
+    uint64_t* k0 = (uint64_t*)talloc((size_t)N * 8);
+    uint64_t* k1 = (uint64_t*)talloc((size_t)N * 8);
+    int* v0 = (int*)talloc((size_t)N * 4);
+    k_morton<<<G, B, 0, st>>>(cen0, box, N, k0, v0);
+    int* sorted = cls ? (int*)talloc((size_t)N * 4) : h.d_cperm;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, k0, k1, v0, sorted, N, 0, 63, st));
+    CK(cub::DeviceRadixSort::SortPairs(scratch(need), need, k0, k1, v0, sorted, N, 0, 63, st));
+    if (cls) {
+      uint8_t* dcls = (uint8_t*)up(cls4.data(), N);
+      uint32_t* c0 = (uint32_t*)k0;
+      uint32_t* c1 = (uint32_t*)k1;
+      k_class_keys<<<G, B, 0, st>>>(sorted, dcls, N, c0, v0);
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, need, c0, c1, v0, h.d_cperm, N, 0, 2, st));
+      CK(cub::DeviceRadixSort::SortPairs(scratch(need), need, c0, c1, v0, h.d_cperm, N, 0, 2, st));
+      tfree(sorted);
+      tfree(dcls);
+    }
+    tfree(k0);
+    tfree(k1);
+    tfree(v0);
+  }
+  int* cinv = (int*)talloc((size_t)N * 4);
+  k_invert<<<G, B, 0, st>>>(h.d_cperm, N, cinv);
+
+  // face order: (touching an owned cell first, internal left cell), stable in id
+  h.F_own = 0;
+  for (int f = 0; f < F; ++f) h.F_own += touch ? (touch[f] ? 1 : 0) : 1;
+  h.d_fperm = dalloc<int>(std::max(1, F));
+  int* finv = (int*)talloc((size_t)F * 4);
+  {
+    uint32_t* k0 = (uint32_t*)talloc((size_t)F * 4);
+    uint32_t* k1 = (uint32_t*)talloc((size_t)F * 4);
+    int* v0 = (int*)talloc((size_t)F * 4);
+    const uint8_t* dtouch = touch ? (const uint8_t*)up(touch, F) : nullptr;
+    k_face_keys<<<G, B, 0, st>>>(fl, cinv, dtouch, N, F, k0, v0);
+    int bits = 1;
+    while (bits < 32 && (2ull * N) >> bits) ++bits;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, k0, k1, v0, h.d_fperm, F, 0, bits, st));
+    CK(cub::DeviceRadixSort::SortPairs(scratch(need), need, k0, k1, v0, h.d_fperm, F, 0, bits, st));
+    tfree(k0);
+    tfree(k1);
+    tfree(v0);
+    if (dtouch) tfree((void*)dtouch);
+  }
+  k_invert<<<G, B, 0, st>>>(h.d_fperm, F, finv);
+
+  // CSR in the reference slot order
+  h.adj_off = dalloc<int>(N + 1);
+  int* count = (int*)talloc((size_t)(N + 1) * 4);
+  CK(cudaMemsetAsync(count, 0, (size_t)(N + 1) * 4, st));
+  {
+    uint64_t* k0 = (uint64_t*)talloc((size_t)F * 16);
+    uint64_t* k1 = (uint64_t*)talloc((size_t)F * 16);
+    int* v0 = (int*)talloc((size_t)F * 8);
+    int* v1 = (int*)talloc((size_t)F * 8);
+    k_slot_keys<<<G, B, 0, st>>>(fl, fr, cinv, finv, F, k0, v0, count);
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, count, h.adj_off, N + 1, st));
+    CK(cub::DeviceScan::ExclusiveSum(scratch(need), need, count, h.adj_off, N + 1, st));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, need, k0, k1, v0, v1, 2 * F, 0, 64, st));
+    CK(cub::DeviceRadixSort::SortPairs(scratch(need), need, k0, k1, v0, v1, 2 * F, 0, 64, st));
+    int M = 0;
+    CK(cudaMemcpyAsync(&M, h.adj_off + N, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h.M = M;
+    h.adj_face = dalloc<int>(std::max(1, M));
+    CK(cudaMemcpyAsync(h.adj_face, v1, (size_t)M * 4, cudaMemcpyDeviceToDevice, st));
+    tfree(k0);
+    tfree(k1);
+    tfree(v0);
+    tfree(v1);
+  }
+  tfree(count);
+
+  // per-face arrays (ledger index of transmissive faces by a scan)
+  const double* fn0 = (const double*)up(mv.face_normal, (size_t)F * 24);
+  const double* fa0 = (const double*)up(mv.face_area, (size_t)F * 8);
+  h.lr = dalloc<int2>(std::max(1, F));
+  h.rcf = h.periodic ? dalloc<int>(F) : nullptr;
+  h.geo = dalloc<double4>(std::max(1, F));
+  h.fcen = dalloc<double>(3 * (size_t)std::max(1, F));
+  {
+    const double* fc0 = (const double*)up(mv.face_centroid, (size_t)F * 24);
+    k_face_arrays<<<G, B, 0, st>>>(h.d_fperm, finv, cinv, fl, fr, fp, fn0, fa0, fc0, F, h.periodic ? 1 : 0,
+                                   h.lr, h.rcf, h.geo, h.fcen);
+    tfree((void*)fc0);
+    int* bflag = (int*)talloc((size_t)(F + 1) * 4);
+    int* bidx = (int*)talloc((size_t)(F + 1) * 4);
+    k_boundary_flags<<<G, B, 0, st>>>(h.d_fperm, fr, fp, F, h.F_own, bflag);
+    CK(cudaMemsetAsync(bflag + F, 0, 4, st));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, need, bflag, bidx, F + 1, st));
+    CK(cub::DeviceScan::ExclusiveSum(scratch(need), need, bflag, bidx, F + 1, st));
+    CK(cudaMemcpyAsync(&h.NB, bidx + F, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    h.bface = dalloc<int>(std::max(1, h.NB));
+    k_boundary_list<<<G, B, 0, st>>>(bflag, bidx, F, h.bface);
+    CK(cudaStreamSynchronize(st));
+    tfree(bflag);
+    tfree(bidx);
+  }
+  h.adj_nb = dalloc<int>(std::max(1, h.M));
+  k_slot_nb<<<G, B, 0, st>>>(h.adj_face, h.lr, h.M, h.adj_nb);
+  k_closure<<<G, B, 0, st>>>(h.adj_off, h.adj_face, h.d_fperm, fn0, fa0, h.n_k1, flags);
+  CK(cudaMemcpyAsync(&hflags, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hflags & 16) throw Error{TAFV_ELOGIC, "mesh: geometric closure violated for a cell"};
+  h.deg6 = !(hflags & 32);
+  tfree((void*)fn0);
+  tfree((void*)fa0);
+
+  // cell arrays
+  h.vol = dalloc<double>(N);
+  h.ivol = dalloc<double>(N);
+  h.chl = dalloc<double>(N);
+  h.cen = dalloc<double>(3 * (size_t)N);
+  k_cell_arrays<<<G, B, 0, st>>>(h.d_cperm, vol0, chl0, cen0, N, h.vol, h.ivol, h.chl, h.cen);
+  if (cls) {
+    h.fint = dalloc<uint8_t>(std::max(1, F));
+    k_face_int<<<G, B, 0, st>>>(h.lr, F, h.n_deep, h.fint);
+  }
+  if (h.deg6) {
+    h.sgeo = dalloc<double4>(std::max(1, h.M));
+    h.sdx = dalloc<double4>(std::max(1, h.M));
+    CK(cudaMemsetAsync(h.sgeo, 0, (size_t)h.M * sizeof(double4), st));
+    CK(cudaMemsetAsync(h.sdx, 0, (size_t)h.M * sizeof(double4), st));
+    k_slot_geo<<<G, B, 0, st>>>(h.adj_face, h.geo, h.fcen, h.cen, h.n_k1, h.sgeo, h.sdx);
+  }
+  h.fdx = dalloc<double4>(2 * (size_t)std::max(1, F));
+  k_face_dx<<<G, B, 0, st>>>(h.lr, h.rcf, h.fcen, h.cen, F, h.periodic ? 1 : 0, h.fdx);
+  CK(cudaGetLastError());
+  // host copies: permutations (boundary calls map ids) and V (internal order)
+  h.cperm.resize(N);
+  h.fperm.resize(F);
+  h.vol_host.resize(N);
+  CK(cudaMemcpyAsync(h.cperm.data(), h.d_cperm, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
+  if (F) CK(cudaMemcpyAsync(h.fperm.data(), h.d_fperm, (size_t)F * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h.vol_host.data(), h.vol, (size_t)N * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
+                 const uint8_t* touch = nullptr) {
+  if (getenv("TAFV_HOST_UPLOAD") != nullptr) upload_mesh_host(h, mv, cls, touch);
+  else upload_mesh_device(h, mv, cls, touch);
 }
 
 void alloc_state(tafv_gpu& h) {
@@ -773,6 +1028,9 @@ void alloc_state(tafv_gpu& h) {
   CK(cudaMallocHost(&h.hplan, sizeof(PlanDev)));
   std::memset(h.hplan, 0, sizeof(PlanDev));
   for (auto& e : h.ev) CK(cudaEventCreate(&e));
+  CK(cudaStreamCreateWithFlags(&h.lst, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&h.ev_led_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h.ev_led, cudaEventDisableTiming));
 }
 
 // Fixed grids for graph capture: every SM filled to the kernel's occupancy.
@@ -1206,6 +1464,29 @@ void inject(tafv_gpu& h, const int32_t* tau_in, double dt, const tafv_options* o
   }
 }
 
+// ---- conservation ledger (k_ledger) on the side stream -----------------------
+// After a corrector's K2 the ledger kernel forks onto `lst` (it reads only
+// int_substep and cadences, which nothing touches until the next corrector's
+// K2); the library stream joins it before that K2 and before k_totals. In a
+// captured sweep the fork / join are graph edges: the ledger is off the
+// critical path.
+template <int NV>
+void ledger_fork(tafv_gpu& h, int level) {
+  if (h.NB == 0) return;
+  CK(cudaEventRecord(h.ev_led_fork, h.st));
+  CK(cudaStreamWaitEvent(h.lst, h.ev_led_fork, 0));
+  const int g = std::max(1, std::min(h.sms * 4, (h.NB + 255) / 256));
+  k_ledger<NV><<<g, 256, 0, h.lst>>>(h.bface, h.NB, h.cad, level, h.isub, (int)h.fs, h.bsum);
+  CK(cudaEventRecord(h.ev_led, h.lst));
+  h.led_pending = true;
+  ++h.launches;
+}
+void ledger_join(tafv_gpu& h) {
+  if (!h.led_pending) return;
+  CK(cudaStreamWaitEvent(h.st, h.ev_led, 0));
+  h.led_pending = false;
+}
+
 // ---- the subiteration sweep ------------------------------------------------
 template <class P, int DEG>
 void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
@@ -1255,6 +1536,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     }, 0, 0, 0);
     ++h.launches;
   }
+  if (!pred) ledger_join(h);  // int_substep is about to be overwritten
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     const int r2 = h.next_dir();
     if (h.sharded()) {  // the faces left after the interior pass
@@ -1265,11 +1547,13 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
       else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, nullptr, 0);
     }
   }, na, nf, nfr);
+  if (!pred) ledger_fork<P::NV>(h, level);
   if (last) {
     timed(h, tafv_gpu::kK3C, [&] {
       k_gather_update<P, false, true, DEG><<<h.nblk_last, 128, 0, h.st>>>(md, sd, nullptr, ncp,
                                                                           h.dplan, h.partials, 0);
     }, na, nf, 0);
+    ledger_join(h);
     k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, h.bsum, h.NB, P::NV);
     h.launches += 4;
     if (h.sharded()) {
@@ -1916,6 +2200,7 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->F_own = h.F_own;
     t->N_global = h.N_global;
     t->NB = h.NB;
+    t->bface = h.bface;
     alloc_state(*t);
     set_grids(*t);
   } catch (...) {
@@ -2187,6 +2472,28 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
                                                                              h->F, h->nv, (int)h->fs, win);
       rows(win, h->F, h->nv, h->d_fperm);
       cudaFree(win);
+    }
+    else if (n == "mesh_digest") {
+      // FNV-1a 64 of every internal mesh array (debug: host vs device build)
+      auto fnv = [&](const void* dptr, size_t bytes) -> uint64_t {
+        std::vector<unsigned char> v(bytes);
+        if (bytes) CK(cudaMemcpy(v.data(), dptr, bytes, cudaMemcpyDeviceToHost));
+        uint64_t x = 1469598103934665603ull;
+        for (unsigned char c : v) x = (x ^ c) * 1099511628211ull;
+        return x;
+      };
+      uint64_t* o = static_cast<uint64_t*>(out);
+      const size_t N = h->N, F = h->F, M = h->M;
+      const void* ptrs[] = {h->vol, h->ivol, h->cen, h->chl, h->adj_off, h->adj_face, h->adj_nb, h->lr,
+                            h->geo, h->fcen, h->sgeo, h->sdx, h->fdx, h->d_cperm, h->d_fperm, h->bface};
+      const size_t sizes[] = {N * 8, N * 8, N * 24, N * 8, (N + 1) * 4, M * 4, M * 4, F * 8,
+                              F * 32, F * 24, h->sgeo ? M * 32 : 0, h->sdx ? M * 32 : 0, F * 64, N * 4, F * 4,
+                              (size_t)h->NB * 4};
+      for (int i = 0; i < 16; ++i) o[i] = ptrs[i] ? fnv(ptrs[i], sizes[i]) : 0;
+      o[16] = (uint64_t)h->M;
+      o[17] = (uint64_t)h->NB;
+      o[18] = (uint64_t)(h->deg6 ? 1 : 0) | (uint64_t)(h->periodic ? 2 : 0);
+      o[19] = h->periodic ? fnv(h->rcf, F * 4) : 0;
     }
     else if (n == "raw_level" || n == "tau") {
       if (n == "raw_level" && h->raw_lazy) materialise_raw(*h);
