@@ -136,6 +136,20 @@ def lib():
     if not os.path.exists(LIB_PATH):
         raise OSError(f"CUDA library missing: {LIB_PATH}; build it with __graft_entry__.build()")
     L = C.CDLL(LIB_PATH)
+    if os.environ.get("TAFV_GPU_LIB"):  # A/B against an older build: bind what it has
+        class _Tolerant:
+            def __init__(self, lib):
+                self.__dict__["_lib"] = lib
+
+            def __getattr__(self, name):
+                try:
+                    return getattr(self._lib, name)
+                except AttributeError:
+                    return type("Missing", (), {"argtypes": None, "restype": None})()
+
+            def __setattr__(self, name, value):
+                setattr(self._lib, name, value)
+        L = _Tolerant(L)
     vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
     L.tafv_gpu_create.argtypes = [C.POINTER(MeshView), C.POINTER(Physics), C.c_int, C.POINTER(vp)]
     L.tafv_gpu_destroy.argtypes = [vp]
