@@ -102,6 +102,10 @@ struct PlanDev {
   long long k1_count[kMaxLevels];    // per-level counts of the deep K1 list
   long long kb_count[kMaxLevels];    // per-level counts of the border K1 list
   long long gcell_count[kMaxLevels]; // owned counts summed over ranks (records, theta)
+  int nfi_prefix[kMaxLevels];        // shards: |{interior f : cadence_f <= l}| (K2 before the halo join)
+  int nfb_prefix[kMaxLevels];        // shards: |{border f touching owned : cadence_f <= l}|
+  long long fi_count[kMaxLevels];
+  long long fb_count[kMaxLevels];
 };
 
 // ---- staging: pure function of the committed/predicted state ---------------
@@ -276,7 +280,11 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       double4 gm;
       double scale;
       if (DEG == 6 && m.sgeo) {
+#ifdef TAFV_EXP_NO_SGEO
+        gm = make_double4(0.5 + 1e-3 * t, 0.25, 0.125, 1e-4 * (t & 7));  // timing experiment only
+#else
         gm = ld4(m.sgeo + t);
+#endif
         scale = gm.w;
       } else {
         const int ef = m.adj_face[t];
@@ -332,7 +340,11 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       for (int t = s0; t < s1; ++t) {
         double dx0, dx1, dx2;
         if (DEG == 6 && m.sdx) {
+#ifdef TAFV_EXP_NO_SDX
+          const double4 d = make_double4(1e-3 * (t & 15), 1e-3, -1e-3, 0.0);  // timing experiment only
+#else
           const double4 d = ld4(m.sdx + t);
+#endif
           dx0 = d.x;
           dx1 = d.y;
           dx2 = d.z;
@@ -405,23 +417,22 @@ __device__ __forceinline__ void load_grad(const StateDev& s, int x, double* g) {
 #ifndef TAFV_K2_MINB
 #define TAFV_K2_MINB 7
 #endif
-template <class P, bool PRED, bool SEL = false>
+// Items: list[i], or base + i (identity: every face of the range active).
+template <class P, bool PRED>
 __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, StateDev s, PhysParams pp,
                                                    const int* __restrict__ list,
-                                                   const int* __restrict__ n_dev, int front,
-                                                   const PlanDev* __restrict__ plan, int rev,
-                                                   const uint8_t* __restrict__ sel, int selv) {
+                                                   const int* __restrict__ n_dev, int base, int front,
+                                                   const PlanDev* __restrict__ plan, int rev) {
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
   const double dt = plan->dt_min;
   const int stride = gridDim.x * blockDim.x;
   for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
     const int i = rev ? n - 1 - ii : ii;
-    const int f = list ? list[i] : i;
     // shards: the pass over the interior faces (both sides deep owned: their
-    // gradients come from the K1 over the deep cells) runs while the halo
-    // is in flight; the other faces after the join (sel = face class)
-    if (SEL && sel[f] != selv) continue;
+    // gradients come from the K1 over the deep cells) runs while the halo is
+    // in flight; the border faces' pass after the join (two lists)
+    const int f = list ? list[i] : base + i;
     const int2 lr = m.lr[f];
     const double4 gm = ld4(m.geo + f);
     const double nrm[3] = {gm.x, gm.y, gm.z};
@@ -916,7 +927,7 @@ struct CompactJob {
   int base;
 };
 struct CompactJobs {
-  CompactJob j[4];
+  CompactJob j[6];
   int njobs;
 };
 

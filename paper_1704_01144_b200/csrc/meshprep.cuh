@@ -108,12 +108,22 @@ __global__ void k_invert(const int* perm, int n, int* inv) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) inv[perm[i]] = i;
 }
 
-// Face order: (not touching an owned cell, internal left cell), stable in
-// original face id.
-__global__ void k_face_keys(const int* fl, const int* cinv, const uint8_t* touch, int N, int F, uint32_t* key,
-                            int* val) {
+// Face order: (touching an owned cell -- shards: interior (both sides deep
+// owned, or a boundary face of a deep cell) before border --, internal left
+// cell), stable in original face id. cls4: 0 deep owned, 1 owned next to the
+// halo, 2 ring 1, 3 ring 2 (null: single domain).
+__global__ void k_face_keys(const int* fl, const int* fr, const int* fp, const int* cinv, const uint8_t* touch,
+                            const uint8_t* cls4, int N, int F, uint32_t* key, int* val) {
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
-    key[f] = (uint32_t)((touch && !touch[f] ? N : 0) + cinv[fl[f]]);
+    int grp = 0;
+    if (touch && !touch[f]) {
+      grp = 2;
+    } else if (cls4) {
+      const int l = fl[f];
+      const int r = fr[f] >= 0 ? fr[f] : fp[f] >= 0 ? fl[fp[f]] : -1;
+      grp = cls4[l] == 0 && (r < 0 || cls4[r] == 0) ? 0 : 1;
+    }
+    key[f] = (uint32_t)grp * (uint32_t)N + (uint32_t)cinv[fl[f]];
     val[f] = f;
   }
 }
@@ -248,12 +258,6 @@ __global__ void k_face_dx(const int2* lr, const int* rcf, const double* fcen, co
     fdx[2 * (size_t)j] = make_double4(dl[0], dl[1], dl[2], 0.0);
     fdx[2 * (size_t)j + 1] = make_double4(dr[0], dr[1], dr[2], 0.0);
   }
-}
-
-// Shards: face class byte (both sides deep owned, or a boundary face of one).
-__global__ void k_face_int(const int2* lr, int F, int n_deep, uint8_t* fint) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x)
-    fint[j] = lr[j].x < n_deep && (lr[j].y < 0 || lr[j].y < n_deep) ? 1 : 0;
 }
 
 }  // namespace prep

@@ -239,7 +239,15 @@ struct tafv_gpu {
   int *d_send_idx = nullptr, *d_recv_idx = nullptr;
   int send_total = 0, recv_total = 0;
   double *sendbuf = nullptr, *recvbuf = nullptr;
-  uint8_t* fint = nullptr;    // shards: [F] 1 = face whose sides are deep owned cells (or boundary of one)
+  // shards: faces [0, F_int) are interior (both sides deep owned, or a
+  // boundary face of a deep cell), [F_int, F_own) the border ones; each
+  // group has its own cadence-sorted K2 list (prefixes nfi / nfb_prefix)
+  int F_int = 0;
+  int* filist = nullptr;
+  int* fblist = nullptr;
+  int* fi_counts = nullptr;
+  int* fb_counts = nullptr;
+  int ntile_fi = 0, ntile_fb = 0;
   int* klist = nullptr;       // K1 list of the deep cells; == clist when single domain
   int* kblist = nullptr;      // K1 list of the border cells (owned next to the halo + ring 1)
   int* k1_counts = nullptr;
@@ -303,7 +311,7 @@ struct tafv_gpu {
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     if (owns_mesh) {
       void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
-                           d_cperm, d_fperm, fint, bface};
+                           d_cperm, d_fperm, bface};
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
@@ -311,7 +319,8 @@ struct tafv_gpu {
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
-                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts};
+                    klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, filist, fblist, fi_counts,
+                    fb_counts};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (hplan) cudaFreeHost(hplan);
@@ -552,14 +561,29 @@ void upload_mesh_host(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls 
   key.clear();
   key.shrink_to_fit();
 
-  // Face order: faces touching an owned cell first; within each group by
-  // internal left cell, stable in original face id.
-  h.F_own = 0;
-  for (int f = 0; f < F; ++f) h.F_own += touch ? (touch[f] ? 1 : 0) : 1;
-  std::vector<int> fstart(2 * (size_t)N + 1, 0);
-  auto fkey = [&](int f) { return (touch && !touch[f] ? N : 0) + cinv[mv.face_left[f]]; };
+  // Face order: faces touching an owned cell first -- on shards the
+  // interior ones (both sides deep owned, or a boundary face of a deep cell:
+  // K2 runs them while the halo is in flight) ahead of the border ones --
+  // then the rest; within each group by internal left cell, stable in
+  // original face id.
+  auto face_interior = [&](int f) {
+    if (!cls) return true;
+    const int l = mv.face_left[f];
+    const int r = mv.face_right[f] >= 0 ? mv.face_right[f]
+                  : mv.face_partner[f] >= 0 ? mv.face_left[mv.face_partner[f]] : -1;
+    return cls4[l] == 0 && (r < 0 || cls4[r] == 0);
+  };
+  h.F_own = h.F_int = 0;
+  for (int f = 0; f < F; ++f) {
+    h.F_own += touch ? (touch[f] ? 1 : 0) : 1;
+    h.F_int += (!touch || touch[f]) && face_interior(f) ? 1 : 0;
+  }
+  std::vector<int> fstart(3 * (size_t)N + 1, 0);
+  auto fkey = [&](int f) {
+    return (touch && !touch[f] ? 2 * N : face_interior(f) ? 0 : N) + cinv[mv.face_left[f]];
+  };
   for (int f = 0; f < F; ++f) ++fstart[fkey(f) + 1];
-  for (int i = 0; i < 2 * N; ++i) fstart[i + 1] += fstart[i];
+  for (int i = 0; i < 3 * N; ++i) fstart[i + 1] += fstart[i];
   h.fperm.resize(F);
   std::vector<int> finv(F);
   {
@@ -641,13 +665,6 @@ void upload_mesh_host(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls 
     for (int d = 0; d < 3; ++d) fcen[3 * (size_t)j + d] = mv.face_centroid[3 * (size_t)f + d];
   }
   h.vol_host = vol;
-  if (cls) {
-    std::vector<uint8_t> fint(F);
-    for (int j = 0; j < F; ++j)
-      fint[j] = lr[j].x < h.n_deep && (lr[j].y < 0 || lr[j].y < h.n_deep) ? 1 : 0;
-    h.fint = dalloc<uint8_t>(std::max(1, F));
-    CK(cudaMemcpy(h.fint, fint.data(), F, cudaMemcpyHostToDevice));
-  }
 
   auto up = [&](auto* dst, const auto& src) {
     CK(cudaMemcpy(dst, src.data(), src.size() * sizeof(src[0]), cudaMemcpyHostToDevice));
@@ -845,9 +862,20 @@ void upload_mesh_device(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cl
   int* cinv = (int*)talloc((size_t)N * 4);
   k_invert<<<G, B, 0, st>>>(h.d_cperm, N, cinv);
 
-  // face order: (touching an owned cell first, internal left cell), stable in id
-  h.F_own = 0;
-  for (int f = 0; f < F; ++f) h.F_own += touch ? (touch[f] ? 1 : 0) : 1;
+  // face order: (touching an owned cell first -- shards: interior ones ahead
+  // of border ones --, internal left cell), stable in id
+  h.F_own = h.F_int = 0;
+  for (int f = 0; f < F; ++f) {
+    const bool t = touch ? touch[f] != 0 : true;
+    h.F_own += t ? 1 : 0;
+    if (t && cls) {
+      const int l = mv.face_left[f];
+      const int r = mv.face_right[f] >= 0 ? mv.face_right[f]
+                    : mv.face_partner[f] >= 0 ? mv.face_left[mv.face_partner[f]] : -1;
+      h.F_int += cls4[l] == 0 && (r < 0 || cls4[r] == 0) ? 1 : 0;
+    }
+  }
+  if (!cls) h.F_int = h.F_own;
   h.d_fperm = dalloc<int>(std::max(1, F));
   int* finv = (int*)talloc((size_t)F * 4);
   {
@@ -855,15 +883,17 @@ void upload_mesh_device(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cl
     uint32_t* k1 = (uint32_t*)talloc((size_t)F * 4);
     int* v0 = (int*)talloc((size_t)F * 4);
     const uint8_t* dtouch = touch ? (const uint8_t*)up(touch, F) : nullptr;
-    k_face_keys<<<G, B, 0, st>>>(fl, cinv, dtouch, N, F, k0, v0);
+    const uint8_t* dcls = cls ? (const uint8_t*)up(cls4.data(), N) : nullptr;
+    k_face_keys<<<G, B, 0, st>>>(fl, fr, fp, cinv, dtouch, dcls, N, F, k0, v0);
     int bits = 1;
-    while (bits < 32 && (2ull * N) >> bits) ++bits;
+    while (bits < 32 && (3ull * N) >> bits) ++bits;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, need, k0, k1, v0, h.d_fperm, F, 0, bits, st));
     CK(cub::DeviceRadixSort::SortPairs(scratch(need), need, k0, k1, v0, h.d_fperm, F, 0, bits, st));
     tfree(k0);
     tfree(k1);
     tfree(v0);
     if (dtouch) tfree((void*)dtouch);
+    if (dcls) tfree((void*)dcls);
   }
   k_invert<<<G, B, 0, st>>>(h.d_fperm, F, finv);
 
@@ -936,10 +966,6 @@ void upload_mesh_device(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cl
   h.chl = dalloc<double>(N);
   h.cen = dalloc<double>(3 * (size_t)N);
   k_cell_arrays<<<G, B, 0, st>>>(h.d_cperm, vol0, chl0, cen0, N, h.vol, h.ivol, h.chl, h.cen);
-  if (cls) {
-    h.fint = dalloc<uint8_t>(std::max(1, F));
-    k_face_int<<<G, B, 0, st>>>(h.lr, F, h.n_deep, h.fint);
-  }
   if (h.deg6) {
     h.sgeo = dalloc<double4>(std::max(1, h.M));
     h.sdx = dalloc<double4>(std::max(1, h.M));
@@ -1018,6 +1044,12 @@ void alloc_state(tafv_gpu& h) {
     h.kblist = dalloc<int>(std::max(1, h.n_k1 - h.n_deep));
     h.ntile_kb = (int)((h.n_k1 - h.n_deep + kTile - 1) / kTile);
     h.kb_counts = dalloc<int>((size_t)std::max(1, h.ntile_kb) * kMaxLevels);
+    h.ntile_fi = (int)((h.F_int + kTile - 1) / kTile);
+    h.ntile_fb = (int)((h.F_own - h.F_int + kTile - 1) / kTile);
+    h.filist = dalloc<int>(std::max(1, h.F_int));
+    h.fblist = dalloc<int>(std::max(1, h.F_own - h.F_int));
+    h.fi_counts = dalloc<int>((size_t)std::max(1, h.ntile_fi) * kMaxLevels);
+    h.fb_counts = dalloc<int>((size_t)std::max(1, h.ntile_fb) * kMaxLevels);
   } else {
     h.klist = h.clist;
   }
@@ -1211,6 +1243,12 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   k_face_cadence<<<std::max(1, (h.F + kTile - 1) / kTile), kCompactThreads, 0, h.st>>>(
       md, h.tau, h.cad, reinterpret_cast<unsigned*>(h.fflag), h.dplan, h.n_own, h.F_own, nkeys, h.face_counts,
       h.ntile_f);
+  if (k1) {  // shards: interior / border face lists
+    k_tile_count<<<std::max(1, h.ntile_fi), kCompactThreads, 0, h.st>>>(h.cad, h.F_int, nkeys, h.fi_counts);
+    k_tile_count<<<std::max(1, h.ntile_fb), kCompactThreads, 0, h.st>>>(h.cad + h.F_int, h.F_own - h.F_int,
+                                                                        nkeys, h.fb_counts);
+    h.launches += 2;
+  }
   // K3 list (owned cells by level), K2 list (faces touching owned by cadence),
   // shards' K1 list: prefixes of each are the active sets of every level
   CompactJobs jobs{};
@@ -1224,7 +1262,11 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
                            &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0], 0};
     jobs.j[3] = CompactJob{h.tau + h.n_deep, h.n_k1 - h.n_deep, std::max(1, h.ntile_kb), h.kb_counts,
                            h.kblist, &h.dplan->kb_count[0], &h.dplan->nkb_prefix[0], h.n_deep};
-    jobs.njobs = 4;
+    jobs.j[4] = CompactJob{h.cad, h.F_int, std::max(1, h.ntile_fi), h.fi_counts, h.filist,
+                           &h.dplan->fi_count[0], &h.dplan->nfi_prefix[0], 0};
+    jobs.j[5] = CompactJob{h.cad + h.F_int, h.F_own - h.F_int, std::max(1, h.ntile_fb), h.fb_counts, h.fblist,
+                           &h.dplan->fb_count[0], &h.dplan->nfb_prefix[0], h.F_int};
+    jobs.njobs = 6;
   }
   int tiles = 0;
   for (int q = 0; q < jobs.njobs; ++q) tiles += jobs.j[q].ntiles;
@@ -1524,8 +1566,10 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   if (h.sharded()) {
     // interior faces while the halo is in flight
     timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
-      if (pred) k_face_flux<P, true, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, 0, h.fint, 1);
-      else k_face_flux<P, false, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, 0, h.fint, 1);
+      const int* fil = all ? nullptr : h.filist;
+      const int* nfip = &h.dplan->nfi_prefix[level];
+      if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fil, nfip, 0, front, cpl, 0);
+      else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fil, nfip, 0, front, cpl, 0);
     }, 0, 0, 0);
     ++h.launches;
     // border cells (owned next to the halo, ring 1) once the halo landed
@@ -1539,12 +1583,15 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   if (!pred) ledger_join(h);  // int_substep is about to be overwritten
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     const int r2 = h.next_dir();
-    if (h.sharded()) {  // the faces left after the interior pass
-      if (pred) k_face_flux<P, true, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, h.fint, 0);
-      else k_face_flux<P, false, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, h.fint, 0);
+    if (h.sharded()) {  // the border faces, after the halo landed
+      const int* fbl = all ? nullptr : h.fblist;
+      const int* nfbp = &h.dplan->nfb_prefix[level];
+      const int gb2 = fixed ? h.grid_k2 : h.grid_for(h.F_own - h.F_int, 128);
+      if (pred) k_face_flux<P, true><<<gb2, 128, 0, h.st>>>(md, sd, h.pp, fbl, nfbp, h.F_int, front, cpl, r2);
+      else k_face_flux<P, false><<<gb2, 128, 0, h.st>>>(md, sd, h.pp, fbl, nfbp, h.F_int, front, cpl, r2);
     } else {
-      if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, nullptr, 0);
-      else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, front, cpl, r2, nullptr, 0);
+      if (pred) k_face_flux<P, true><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, 0, front, cpl, r2);
+      else k_face_flux<P, false><<<g2, 128, 0, h.st>>>(md, sd, h.pp, fl, nfp, 0, front, cpl, r2);
     }
   }, na, nf, nfr);
   if (!pred) ledger_fork<P::NV>(h, level);
@@ -2198,6 +2245,7 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->n_own = h.n_own;
     t->n_k1 = h.n_k1;
     t->F_own = h.F_own;
+    t->F_int = h.F_int;
     t->N_global = h.N_global;
     t->NB = h.NB;
     t->bface = h.bface;
