@@ -1563,7 +1563,12 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
   }, na, nf, nfr);
   const PlanDev* cpl = h.dplan;
-  if (h.sharded()) {
+  // shards with a halo: deep / border K1 lists and interior / border K2
+  // lists (a shard without halo cells -- one rank -- runs the single-domain
+  // lists and only joins the (empty) exchange)
+  const bool split = h.sharded() && h.klist != h.clist;
+  if (h.sharded() && !split) halo_join(h);
+  if (split) {
     // interior faces while the halo is in flight
     timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
       const int* fil = all ? nullptr : h.filist;
@@ -1583,7 +1588,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   if (!pred) ledger_join(h);  // int_substep is about to be overwritten
   timed(h, pred ? tafv_gpu::kK2P : tafv_gpu::kK2C, [&] {
     const int r2 = h.next_dir();
-    if (h.sharded()) {  // the border faces, after the halo landed
+    if (split) {  // the border faces, after the halo landed
       const int* fbl = all ? nullptr : h.fblist;
       const int* nfbp = &h.dplan->nfb_prefix[level];
       const int gb2 = fixed ? h.grid_k2 : h.grid_for(h.F_own - h.F_int, 128);
