@@ -202,7 +202,8 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
  * "w_pred" [nc][nv], "grad" [nc][nv][3], "phi_pred" / "int_substep" /
  * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32);
  * "mesh_digest" [20] (uint64: FNV-1a of every internal mesh array, slot
- * count, boundary count, flags -- compares the device and host builds). */
+ * count, boundary count, flags -- compares the device and host builds);
+ * "repartition_ms" [1] (double: wall time of the last repartition). */
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
 
 /* Launch configuration knobs (bench/profiling):
@@ -272,6 +273,27 @@ void tafv_comm_destroy(tafv_comm* comm);
 int tafv_gpu_create_shard(const tafv_mesh_view* global_mesh, const tafv_physics* physics, int device,
                           const int32_t* rank_of_cell, int32_t rank, tafv_comm* comm,
                           tafv_gpu** out);
+
+/* DistDriver::repartition (exchange.cpp:595-609), collective over the
+ * shard's communicator, in place (the handle pointer stays valid): the
+ * ranks all-reduce their owned rows of the committed state and the last
+ * plan's level map, cut a new partition -- `rank_of_cell` if given, else
+ * contiguous slabs along `axis` balancing the level cost 2^(theta - tau)
+ * (exchange.cpp:598-603) -- and rebuild the shard on the device from
+ * `global_mesh` (the mesh the shard was created from; the caller keeps it,
+ * as DistDriver keeps its `const Mesh&`). State, t0 and iteration carry over
+ * bitwise. rank_of_cell_out (optional, [n_cells]) receives the partition.
+ * logic_error (TAFV_ELOGIC) before any plan, as the reference. On a failure
+ * after the rebuild started the handle must be destroyed. */
+int tafv_gpu_repartition(tafv_gpu* h, const tafv_mesh_view* global_mesh, const int32_t* rank_of_cell,
+                         int32_t axis, int32_t* rank_of_cell_out);
+
+/* DistOptions::repartition_every (exchange.hpp:140-143): tafv_gpu_iterate
+ * repartitions the shard (level-cost slabs along `axis`) before iteration i
+ * whenever i > 0 and i % every == 0, as DistDriver::integrate does
+ * (exchange.cpp:611-618). every = 0 switches it off. `global_mesh` must
+ * outlive the setting. */
+int tafv_gpu_set_repartition(tafv_gpu* h, const tafv_mesh_view* global_mesh, int32_t every, int32_t axis);
 
 /* ---- formats (host only) ----------------------------
  * TFVM mesh files: version 1 = the reference's 2D format (Mesh::save,

@@ -109,7 +109,7 @@ EXPORTS = [
     "tafv_gpu_set_flag", "tafv_gpu_stats", "tafv_gpu_kernel_times", "tafv_gpu_mesh_info", "tafv_mesh_hex", "tafv_mesh_hex_window",
     "tafv_partition_slabs", "tafv_shard_describe", "tafv_level_smooth", "tafv_shard_last_error",
     "tafv_comm_nccl_unique_id", "tafv_comm_create_nccl", "tafv_comm_create_loopback",
-    "tafv_comm_destroy", "tafv_gpu_create_shard",
+    "tafv_comm_destroy", "tafv_gpu_create_shard", "tafv_gpu_repartition", "tafv_gpu_set_repartition",
     "tafv_mesh_save", "tafv_mesh_load", "tafv_mesh_hash", "tafv_snapshot_save", "tafv_snapshot_load",
     "tafv_snapshot_compare", "tafv_io_last_error",
 ]
@@ -183,6 +183,8 @@ def lib():
     L.tafv_comm_destroy.restype = None
     L.tafv_gpu_create_shard.argtypes = [C.POINTER(MeshView), C.POINTER(Physics), C.c_int, vp, i32, vp,
                                         C.POINTER(vp)]
+    L.tafv_gpu_repartition.argtypes = [vp, C.POINTER(MeshView), vp, i32, vp]
+    L.tafv_gpu_set_repartition.argtypes = [vp, C.POINTER(MeshView), i32, i32]
     L.tafv_mesh_save.argtypes = [C.c_char_p, C.POINTER(MeshView)]
     L.tafv_mesh_load.argtypes = [C.c_char_p, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)] + [vp] * 9
     L.tafv_mesh_hash.argtypes = [C.POINTER(MeshView)]

@@ -155,6 +155,9 @@ class Solver:
                                                 comm.h, C.byref(h))
             self.rank = int(rank)
             self.owned = self._roc == self.rank
+            # the GLOBAL mesh view stays alive for in-library repartitions
+            # (DistDriver keeps its const Mesh&)
+            self._mesh_arrs, self._mv = arrs, mv
         if rc != 0:
             raise _EXC.get(rc, TafvError)(self.lib.tafv_gpu_last_error(None).decode())
         self.h = h
@@ -188,6 +191,28 @@ class Solver:
             if a is not None and a.size != self.nc * self.nv:
                 raise InvalidArgument("set_state: wrong state size")
         self._c(self.lib.tafv_gpu_set_state(self.h, _ptr(wa), _ptr(Wa), float(t0), int(iteration)))
+
+    def repartition(self, rank_of_cell=None, axis=0):
+        """DistDriver::repartition (exchange.cpp:595-609), collective over
+        the shard's ranks, in place (tafv_gpu_repartition): the committed
+        state migrates, the shard is rebuilt on the device. rank_of_cell=None:
+        level-cost slabs along `axis` from the last plan. Returns the
+        partition now in force."""
+        if not hasattr(self, "_mv"):
+            raise InvalidArgument("repartition: not a shard")
+        roc = None if rank_of_cell is None else np.ascontiguousarray(rank_of_cell, dtype=np.int32)
+        out = np.empty(self.nc, dtype=np.int32)
+        self._c(self.lib.tafv_gpu_repartition(self.h, C.byref(self._mv), _ptr(roc), int(axis), _ptr(out)))
+        self._roc = out
+        self.owned = out == self.rank
+        return out
+
+    def set_repartition(self, every, axis=0):
+        """DistOptions::repartition_every: reference_integrate repartitions
+        by level cost every `every` iterations (0: off)."""
+        if not hasattr(self, "_mv"):
+            raise InvalidArgument("set_repartition: not a shard")
+        self._c(self.lib.tafv_gpu_set_repartition(self.h, C.byref(self._mv), int(every), int(axis)))
 
     def get_state(self):
         """(w, W, t0, iteration); a shard fills only its owned rows (zeros elsewhere)."""
@@ -265,6 +290,8 @@ class Solver:
             out = np.zeros(self.nc, dtype=np.int32)
         elif name == "mesh_digest":
             out = np.zeros(20, dtype=np.uint64)
+        elif name == "repartition_ms":
+            out = np.zeros(1)
         else:
             rows = self.nf if name in ("phi_pred", "int_substep", "int_window") else self.nc
             width = {"grad": self.nv * 3, "dt_max": 1}.get(name, self.nv)

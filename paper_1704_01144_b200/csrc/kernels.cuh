@@ -106,6 +106,7 @@ struct PlanDev {
   int nfb_prefix[kMaxLevels];        // shards: |{border f touching owned : cadence_f <= l}|
   long long fi_count[kMaxLevels];
   long long fb_count[kMaxLevels];
+  int sweep_changed[kMaxLevels];     // single-domain plan: Jacobi sweep i changed a level
 };
 
 // ---- staging: pure function of the committed/predicted state ---------------
@@ -654,39 +655,60 @@ __global__ void __launch_bounds__(256) k_ledger(const int* __restrict__ bface, i
   }
 }
 
-// Fixed-order reduction of the per-block partials: block k reduces
-// component k (deterministic tree over a fixed number of partials). The same
-// block reduces the ledger's per-face boundary outflows of component k
-// (compensated, fixed shape) into plan->bflux[k] and clears them for the
-// next iteration.
-__global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan, double* bsum,
-                                                int nb, int nv) {
+// The ledger's per-face boundary outflows into per-block compensated
+// partials: block g reduces faces [g*per, (g+1)*per) (fixed shape, so the
+// sum is deterministic) component by component, clears them for the next
+// iteration and leaves lpart[k][g]. Spread over the whole device: one block
+// per component walking ~10^6 faces cost ~3 ms per iteration on config 4.
+template <int NV>
+__global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD* lpart) {
   __shared__ DD red[256];
-  const int k = blockIdx.x;
+  const int per = (nb + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
+#pragma unroll 1
+  for (int k = 0; k < NV; ++k) {
+    DD o{0.0, 0.0};
+    for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+      double* p = bsum + (size_t)b * NV + k;
+      o = dd_add(o, *p);
+      *p = 0.0;
+    }
+    red[threadIdx.x] = o;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) lpart[(size_t)k * gridDim.x + blockIdx.x] = red[0];
+    __syncthreads();
+  }
+}
+
+// Fixed-order reduction of the per-block partials: block k reduces
+// component k (deterministic tree over a fixed number of partials) of the
+// state totals and, when the ledger runs, of its boundary outflows
+// (k_ledger_reduce's partials) into plan->bflux[k].
+__device__ __forceinline__ DD block_merge(const DD* part, int n, DD* red) {
   DD a{0.0, 0.0};
-  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) a = dd_merge(a, partials[(size_t)k * nblocks + b]);
+  for (int b = threadIdx.x; b < n; b += blockDim.x) a = dd_merge(a, part[b]);
   red[threadIdx.x] = a;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
     __syncthreads();
   }
-  if (threadIdx.x == 0) plan->totals[k] = red[0].hi + red[0].lo;
+  const DD r = red[0];
   __syncthreads();
-  DD o{0.0, 0.0};
-  if (bsum)
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-      double* p = bsum + (size_t)b * nv + k;
-      o = dd_add(o, *p);
-      *p = 0.0;
-    }
-  red[threadIdx.x] = o;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) plan->bflux[k] = red[0].hi + red[0].lo;
+  return r;
+}
+__global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan, const DD* lpart,
+                                                int nl) {
+  __shared__ DD red[256];
+  const int k = blockIdx.x;
+  const DD t = block_merge(partials + (size_t)k * nblocks, nblocks, red);
+  if (threadIdx.x == 0) plan->totals[k] = t.hi + t.lo;
+  const DD o = lpart ? block_merge(lpart + (size_t)k * nl, nl, red) : DD{0.0, 0.0};
+  if (threadIdx.x == 0) plan->bflux[k] = o.hi + o.lo;
 }
 
 // ---- plan kernels ----------------------------------------------------------
@@ -750,6 +772,8 @@ __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParam
   }
   if (reset)
     for (int i = threadIdx.x; i < 3 * kMaxLevels; i += blockDim.x) (&plan->cell_count[0])[i] = 0;
+  if (reset)
+    for (int i = threadIdx.x; i < kMaxLevels; i += blockDim.x) plan->sweep_changed[i] = 0;
 }
 
 // levels.cpp:18-25: raw = ratio >= 1 ? ilogb(ratio) : 0, clamped.
@@ -808,10 +832,10 @@ constexpr int kCompactThreads = 256;
 // flags of the cells swept are cleared for k_face_cadence.
 template <bool FIRST, bool COUNT>
 __global__ void __launch_bounds__(kCompactThreads) k_level_sweep(MeshDev m, const int8_t* in,
-                                                                 const double* dt_max, const PlanDev* plan,
+                                                                 const double* dt_max, PlanDev* plan,
                                                                  int theta_max, int smooth, int8_t* out,
                                                                  int n, int nkeys, int* counts,
-                                                                 uint8_t* clear_flag) {
+                                                                 uint8_t* clear_flag, int sweep) {
   double dt_min = 0.0, y = 0.0;
   bool ok = false;
   if (FIRST) {
@@ -823,17 +847,23 @@ __global__ void __launch_bounds__(kCompactThreads) k_level_sweep(MeshDev m, cons
     if (FIRST) return ok ? classify_raw(dt_max[x], dt_min, y, theta_max) : 0;
     return in[x];
   };
+  // Jacobi converged: the previous sweep changed no level, so this one would
+  // not either -- copy its input (the fixpoint) instead of re-reading the
+  // adjacency (sweeps after the fixpoint cost 2 bytes per cell, not ~30)
+  const bool done = !FIRST && plan->sweep_changed[sweep - 1] == 0;
   __shared__ int cnt[kMaxLevels];
   if (COUNT) {
     if (threadIdx.x < kMaxLevels) cnt[threadIdx.x] = 0;
     __syncthreads();
   }
+  bool changed = false;
   const int beg = COUNT ? blockIdx.x * kTile + threadIdx.x : blockIdx.x * blockDim.x + threadIdx.x;
   const int end = COUNT ? min(n, (int)(blockIdx.x + 1) * kTile) : n;
   const int step = COUNT ? blockDim.x : gridDim.x * blockDim.x;
   for (int c = beg; c < end; c += step) {
-    int bound = lev(c);
-    if (smooth) {
+    const int own = lev(c);
+    int bound = own;
+    if (smooth && !done) {
       const int s0 = m.adj_off[c], s1 = m.adj_off[c + 1];
       for (int t = s0; t < s1; ++t) {
         const int nb = m.adj_nb[t];
@@ -843,10 +873,12 @@ __global__ void __launch_bounds__(kCompactThreads) k_level_sweep(MeshDev m, cons
         }
       }
     }
+    changed |= bound != own;
     out[c] = (int8_t)bound;
     if (clear_flag) clear_flag[c] = 0;
     if (COUNT) atomicAdd(&cnt[bound], 1);
   }
+  if (__any_sync(0xffffffffu, changed) && (threadIdx.x & 31) == 0) atomicOr(&plan->sweep_changed[sweep], 1);
   if (COUNT) {
     __syncthreads();
     if (threadIdx.x < nkeys) counts[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = cnt[threadIdx.x];
@@ -934,39 +966,58 @@ struct CompactJobs {
 // Exclusive scan of each job's counts in (key, tile) order, in place; block b
 // scans job b, writes its per-key totals and their prefix sums. Block 0 (the
 // K3 cell list) also publishes the record counts and, for a single domain,
-// aliases the K1 list to it.
+// aliases the K1 list to it. Each warp scans a contiguous segment 32 entries
+// at a time (coalesced, shuffle scan, running carry), then the warp offsets
+// are added: ~10^6 counts (config 4's face tiles) in ~20 us instead of the
+// 0.6 ms of per-thread sequential segments.
 __global__ void __launch_bounds__(1024) k_tile_scan(CompactJobs jobs, int nkeys, PlanDev* plan,
                                                     int alias_k1) {
   const CompactJob jb = jobs.j[blockIdx.x];
   int* counts = jb.counts;
   const int ntiles = jb.ntiles;
   const int total = ntiles * nkeys;
-  const int per = (total + blockDim.x - 1) / blockDim.x;
-  const int b = threadIdx.x * per, e = min(total, b + per);
-  int local = 0;
-  for (int i = b; i < e; ++i) local += counts[i];
-  __shared__ int part[1024];
-  part[threadIdx.x] = local;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int per = (total + nw - 1) / nw;
+  const int b = min(total, warp * per), e = min(total, b + per);
+  int carry = 0;
+  for (int base = b; base < e; base += 32) {
+    const int i = base + lane;
+    const int v = i < e ? counts[i] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < e) counts[i] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  __shared__ int wofs[32];
+  __shared__ int grand;
+  if (lane == 0) wofs[warp] = carry;
   __syncthreads();
-  for (int off = 1; off < blockDim.x; off <<= 1) {
-    const int v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
-    __syncthreads();
-    part[threadIdx.x] += v;
-    __syncthreads();
+  if (warp == 0) {
+    const int v = lane < nw ? wofs[lane] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    wofs[lane] = x - v;
+    if (lane == 31) grand = x;
   }
-  int run = part[threadIdx.x] - local;
-  for (int i = b; i < e; ++i) {
-    const int v = counts[i];
-    counts[i] = run;
-    run += v;
-  }
+  __syncthreads();
+  const int off = wofs[warp];
+  if (off)
+    for (int i = b + lane; i < e; i += 32) counts[i] += off;
   __syncthreads();
   // per-key totals: next key's first offset minus this key's first offset
   if (threadIdx.x < nkeys) {
     long long t = 0;
     if (ntiles > 0) {
       const int first = counts[(size_t)threadIdx.x * ntiles];
-      const int next = threadIdx.x + 1 < nkeys ? counts[(size_t)(threadIdx.x + 1) * ntiles] : part[blockDim.x - 1];
+      const int next = threadIdx.x + 1 < nkeys ? counts[(size_t)(threadIdx.x + 1) * ntiles] : grand;
       t = next - first;
     }
     jb.totals[threadIdx.x] = t;

@@ -32,6 +32,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <cstdint>
+#include <chrono>
 #include <cstring>
 #include <array>
 #include <map>
@@ -107,6 +108,13 @@ struct tafv_gpu {
   std::string err;
   int model = TAFV_EULER, nv = 5, dim = 3;
   PhysParams pp{};
+  tafv_physics phys{};  // as created (in-place rebuilds)
+  bool levels_made = false;  // a plan has been made (device tau = the last plan's levels)
+  // DistDriver's repartition_every (exchange.hpp:140-143): tafv_gpu_iterate
+  // repartitions shards by level cost every `rep_every` iterations
+  const tafv_mesh_view* rep_mesh = nullptr;
+  int rep_every = 0, rep_axis = 0;
+  double rep_ms = 0.0;  // wall time of the last repartition
   int N = 0, F = 0, M = 0;
   bool periodic = false;
   int sms = 148;
@@ -153,6 +161,7 @@ struct tafv_gpu {
   double4* sdx = nullptr;
   double4* fdx = nullptr;  // see MeshDev::fdx
   bool slot_geo = true;
+  bool slot_n = true, slot_dx = true;  // A/B: per-slot normals / limiter offsets individually
   bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
   // run_batch lanes: a twin handle sharing this one's (read-only) mesh arrays
@@ -173,6 +182,8 @@ struct tafv_gpu {
   int NB = 0;
   int* bface = nullptr;       // [NB] internal face ids (mesh, shared with the twin)
   double* bsum = nullptr;     // [NB][nv] running outflow since the last trailing corrector
+  DD* lpart = nullptr;        // [nv][nblk_led] per-block partials of the outflow (k_ledger_reduce)
+  int nblk_led = 1;
   cudaStream_t lst = nullptr; // side stream of the ledger kernels
   cudaEvent_t ev_led_fork = nullptr, ev_led = nullptr;
   bool led_pending = false;
@@ -277,8 +288,8 @@ struct tafv_gpu {
 
   MeshDev mesh_dev() const {
     return MeshDev{N,    F,   vol,    ivol,   cen,  chl, adj_off, adj_face, adj_nb, lr,
-                   periodic ? rcf : nullptr, geo, fcen, slot_geo ? sgeo : nullptr,
-                   slot_geo ? sdx : nullptr, face_dx ? fdx : nullptr};
+                   periodic ? rcf : nullptr, geo, fcen, slot_geo && slot_n ? sgeo : nullptr,
+                   slot_geo && slot_dx ? sdx : nullptr, face_dx ? fdx : nullptr};
   }
   StateDev state_dev() const {
     return StateDev{w, W, wp, grad, tau, cad, phi, isub, iwin, iwin_alias ? ialias : nullptr};
@@ -299,7 +310,10 @@ struct tafv_gpu {
     return (int)std::min<long long>(g, grid_cap);
   }
 
-  ~tafv_gpu() {
+  ~tafv_gpu() { release(); }
+  // Frees every device / host resource (destructor; in-place rebuild of a
+  // repartitioned shard, tafv_gpu_repartition).
+  void release() {
     cudaSetDevice(device);
     delete twin;
     for (auto& g : graphs) {
@@ -315,7 +329,7 @@ struct tafv_gpu {
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
-    void* ptrs[] = {w,     W,        wp,       bsum,
+    void* ptrs[] = {w,     W,        wp,       bsum,  lpart,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
@@ -1014,6 +1028,8 @@ void alloc_state(tafv_gpu& h) {
   CK(cudaMemset(h.ialias, 0, F));
   h.bsum = dalloc<double>(std::max<size_t>(1, (size_t)h.NB * nv));
   CK(cudaMemset(h.bsum, 0, std::max<size_t>(1, (size_t)h.NB * nv) * sizeof(double)));
+  h.nblk_led = (int)std::max<long long>(1, std::min<long long>(2LL * h.sms, ((long long)h.NB + 1023) / 1024));
+  h.lpart = dalloc<DD>((size_t)nv * h.nblk_led);
   h.tau = dalloc<int8_t>(N);
   h.raw = dalloc<int8_t>(N);
   h.tmpa = dalloc<int8_t>(N);
@@ -1409,16 +1425,16 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
       uint8_t* clr = first ? h.fflag : nullptr;
       if (first && last)
         k_level_sweep<true, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
       else if (first)
         k_level_sweep<true, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
       else if (last)
         k_level_sweep<false, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
       else
         k_level_sweep<false, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
       ++h.launches;
       src = dst;
     }
@@ -1450,6 +1466,7 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
 // (reference.cpp:93).
 void check_plan(tafv_gpu& h) {
   accept_plan(h);
+  h.levels_made = true;
   if (!(std::isfinite(h.dt) && h.dt > 0.0)) {
     h.has_plan = false;
     throw Error{TAFV_EINVAL, "integrate: stable step collapsed"};
@@ -1606,7 +1623,11 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
                                                                           h.dplan, h.partials, 0);
     }, na, nf, 0);
     ledger_join(h);
-    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, h.bsum, h.NB, P::NV);
+    if (h.NB) {
+      k_ledger_reduce<P::NV><<<h.nblk_led, 256, 0, h.st>>>(h.bsum, h.NB, h.lpart);
+      ++h.launches;
+    }
+    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, h.NB ? h.lpart : nullptr, h.nblk_led);
     h.launches += 4;
     if (h.sharded()) {
       h.comm->allreduce_sum_f64(h.rank, h.dplan->totals, P::NV, h.st);
@@ -1823,6 +1844,86 @@ extern "C" {
 
 // Shared by tafv_gpu_create and tafv_gpu_create_shard. `shard` (optional)
 // makes the handle a rank of a decomposed run.
+// Builds a handle's device resources in place (throws). `shard` (optional)
+// makes the handle a rank of a decomposed run. Shared by tafv_gpu_create,
+// tafv_gpu_create_shard and the in-place rebuild of tafv_gpu_repartition.
+static void init_handle(tafv_gpu* h, const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
+                        const tafv::Shard* shard, tafv_comm* comm, int n_global) {
+  h->device = device;
+  h->phys = *physics;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&h->cst, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+  }
+  CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
+  h->grid_cap = h->sms * 16;
+  h->model = physics->model;
+  switch (physics->model) {
+    case TAFV_ADVECTION:
+      h->nv = 1;
+      h->pp.ax = physics->a[0];
+      h->pp.ay = physics->a[1];
+      break;
+    case TAFV_BURGERS: {  // parse_flux_model (physics.cpp:13-17)
+      h->nv = 1;
+      const double len = std::sqrt(physics->a[0] * physics->a[0] + physics->a[1] * physics->a[1]);
+      require(len > 0.0, "physics: burgers direction must be nonzero");
+      h->pp.ax = physics->a[0] / len;
+      h->pp.ay = physics->a[1] / len;
+      break;
+    }
+    case TAFV_EULER:
+      require(physics->gamma > 1.0, "physics: gamma must exceed 1");
+      h->nv = 5;
+      h->pp.gamma = physics->gamma;
+      h->pp.gm1 = physics->gamma - 1.0;
+      break;
+    default:
+      require(false, "physics: unknown model");
+  }
+  if (h->model != TAFV_EULER) require(mesh->dim <= 2, "physics: scalar models run on 1D/2D meshes");
+  else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
+  if (shard) {
+    std::vector<uint8_t> touch(shard->touch_own.begin(), shard->touch_own.end());
+    upload_mesh(*h, *mesh, shard->cls.data(), touch.data());
+    h->comm = comm;
+    h->rank = shard->rank;
+    h->nranks = shard->nranks;
+    h->N_global = n_global;
+    h->shard_cells = shard->cells;
+    // exchange lists in internal ids, peer segments in shard order
+    std::vector<int> cinv(h->N);
+    for (int i = 0; i < h->N; ++i) cinv[h->cperm[i]] = i;
+    std::vector<int> sidx, ridx;
+    for (size_t p = 0; p < shard->peers.size(); ++p) {
+      tafv_gpu::Peer pe{shard->peers[p], (int)shard->send[p].size(), (int)shard->recv[p].size(),
+                        (int)sidx.size(), (int)ridx.size()};
+      for (int c : shard->send[p]) sidx.push_back(cinv[c]);
+      for (int c : shard->recv[p]) ridx.push_back(cinv[c]);
+      h->peers.push_back(pe);
+    }
+    h->send_total = (int)sidx.size();
+    h->recv_total = (int)ridx.size();
+    h->d_send_idx = dalloc<int>(sidx.size());
+    h->d_recv_idx = dalloc<int>(ridx.size());
+    if (!sidx.empty()) CK(cudaMemcpy(h->d_send_idx, sidx.data(), sidx.size() * 4, cudaMemcpyHostToDevice));
+    if (!ridx.empty()) CK(cudaMemcpy(h->d_recv_idx, ridx.data(), ridx.size() * 4, cudaMemcpyHostToDevice));
+    const int width = std::max(h->nv, 1);
+    h->sendbuf = dalloc<double>((size_t)std::max(1, h->send_total) * width);
+    h->recvbuf = dalloc<double>((size_t)std::max(1, h->recv_total) * width);
+    comm->attach(h->rank, h);
+  } else {
+    upload_mesh(*h, *mesh);
+  }
+  alloc_state(*h);
+  set_grids(*h);
+}
+
 static int create_handle(const tafv_mesh_view* mesh, const tafv_physics* physics, int device,
                          const tafv::Shard* shard, tafv_comm* comm, int n_global, tafv_gpu** out) {
   if (!out || !mesh || !physics) {
@@ -1833,77 +1934,7 @@ static int create_handle(const tafv_mesh_view* mesh, const tafv_physics* physics
   auto* h = new tafv_gpu;
   h->device = device;
   try {
-    CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
-    {
-      int lo = 0, hi = 0;
-      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CK(cudaStreamCreateWithPriority(&h->cst, cudaStreamNonBlocking, hi));
-      CK(cudaEventCreateWithFlags(&h->ev_pack, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
-    }
-    CK(cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device));
-    h->grid_cap = h->sms * 16;
-    h->model = physics->model;
-    switch (physics->model) {
-      case TAFV_ADVECTION:
-        h->nv = 1;
-        h->pp.ax = physics->a[0];
-        h->pp.ay = physics->a[1];
-        break;
-      case TAFV_BURGERS: {  // parse_flux_model (physics.cpp:13-17)
-        h->nv = 1;
-        const double len = std::sqrt(physics->a[0] * physics->a[0] + physics->a[1] * physics->a[1]);
-        require(len > 0.0, "physics: burgers direction must be nonzero");
-        h->pp.ax = physics->a[0] / len;
-        h->pp.ay = physics->a[1] / len;
-        break;
-      }
-      case TAFV_EULER:
-        require(physics->gamma > 1.0, "physics: gamma must exceed 1");
-        h->nv = 5;
-        h->pp.gamma = physics->gamma;
-        h->pp.gm1 = physics->gamma - 1.0;
-        break;
-      default:
-        require(false, "physics: unknown model");
-    }
-    if (h->model != TAFV_EULER) require(mesh->dim <= 2, "physics: scalar models run on 1D/2D meshes");
-    else require(mesh->dim == 3, "physics: Euler runs on 3D meshes");
-    if (shard) {
-      std::vector<uint8_t> touch(shard->touch_own.begin(), shard->touch_own.end());
-      upload_mesh(*h, *mesh, shard->cls.data(), touch.data());
-      h->comm = comm;
-      h->rank = shard->rank;
-      h->nranks = shard->nranks;
-      h->N_global = n_global;
-      h->shard_cells = shard->cells;
-      // exchange lists in internal ids, peer segments in shard order
-      std::vector<int> cinv(h->N);
-      for (int i = 0; i < h->N; ++i) cinv[h->cperm[i]] = i;
-      std::vector<int> sidx, ridx;
-      for (size_t p = 0; p < shard->peers.size(); ++p) {
-        tafv_gpu::Peer pe{shard->peers[p], (int)shard->send[p].size(), (int)shard->recv[p].size(),
-                          (int)sidx.size(), (int)ridx.size()};
-        for (int c : shard->send[p]) sidx.push_back(cinv[c]);
-        for (int c : shard->recv[p]) ridx.push_back(cinv[c]);
-        h->peers.push_back(pe);
-      }
-      h->send_total = (int)sidx.size();
-      h->recv_total = (int)ridx.size();
-      h->d_send_idx = dalloc<int>(sidx.size());
-      h->d_recv_idx = dalloc<int>(ridx.size());
-      if (!sidx.empty()) CK(cudaMemcpy(h->d_send_idx, sidx.data(), sidx.size() * 4, cudaMemcpyHostToDevice));
-      if (!ridx.empty()) CK(cudaMemcpy(h->d_recv_idx, ridx.data(), ridx.size() * 4, cudaMemcpyHostToDevice));
-      const int width = std::max(h->nv, 1);
-      h->sendbuf = dalloc<double>((size_t)std::max(1, h->send_total) * width);
-      h->recvbuf = dalloc<double>((size_t)std::max(1, h->recv_total) * width);
-      comm->attach(h->rank, h);
-    } else {
-      upload_mesh(*h, *mesh);
-    }
-    alloc_state(*h);
-    set_grids(*h);
+    init_handle(h, mesh, physics, device, shard, comm, n_global);
   } catch (const Error& e) {
     g_create_error = e.what;
     delete h;
@@ -2131,10 +2162,158 @@ int tafv_gpu_run_iteration(tafv_gpu* h, tafv_record* out) {
   });
 }
 
+// ---- in-library repartition (DistDriver::repartition, exchange.cpp:595-609)
+// Every rank publishes its owned rows of W (as bit patterns, so the sum
+// with the other ranks' zeros is exact, signed zeros included) and its owned
+// cells' levels into global device buffers; all-reduces over the shard
+// communicator give every rank the global committed state and the last
+// plan's level map (the reference's sync_doubles of w / W); the level cost
+// 2^(theta - tau) cuts new slabs (exchange.cpp:598-603) unless the caller
+// passes a partition; the handle is rebuilt IN PLACE from the global mesh
+// (shard description, device mesh build, state, graphs) and restored to the
+// same W (w = W / V, the relation every corrector leaves), t0 and iteration.
+__global__ void k_publish_owned(const double* __restrict__ W, const int8_t* __restrict__ tau,
+                                const int* __restrict__ gid, int n_own, int nv, long long* gW, int* gtau) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_own; i += gridDim.x * blockDim.x) {
+    const size_t g = (size_t)gid[i];
+    for (int k = 0; k < nv; ++k) gW[g * nv + k] = __double_as_longlong(W[(size_t)i * nv + k]);
+    gtau[g] = tau[i];
+  }
+}
+
+static void repartition(tafv_gpu* h, const tafv_mesh_view* gm, const int32_t* roc_in, int axis,
+                        int32_t* roc_out) {
+  const auto t_start = std::chrono::steady_clock::now();
+  require(h->sharded(), "repartition: the handle is not a shard (tafv_gpu_create_shard)");
+  require(gm != nullptr && gm->n_cells == h->N_global, "repartition: global mesh differs from the shard's");
+  if (!h->levels_made) throw Error{TAFV_ELOGIC, "dist: repartition before any iteration"};
+  require(h->state_set, "repartition: no state");
+  const int NG = h->N_global, nv = h->nv;
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->st));
+  // 1. global committed state and last plan's levels on every rank
+  std::vector<int> gid(h->n_own);
+  for (int i = 0; i < h->n_own; ++i) gid[i] = h->shard_cells[h->cperm[i]];
+  int* dgid = dalloc<int>(std::max(1, h->n_own));
+  long long* gWb = dalloc<long long>((size_t)NG * nv);
+  int* gtau = dalloc<int>(NG);
+  std::vector<long long> hW((size_t)NG * nv);
+  std::vector<int> htau(NG);
+  try {
+    if (h->n_own) CK(cudaMemcpy(dgid, gid.data(), gid.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemsetAsync(gWb, 0, (size_t)NG * nv * 8, h->st));
+    CK(cudaMemsetAsync(gtau, 0xff, (size_t)NG * 4, h->st));
+    k_publish_owned<<<h->grid_for(h->n_own, 256), 256, 0, h->st>>>(h->W, h->tau, dgid, h->n_own, nv, gWb, gtau);
+    CK(cudaGetLastError());
+    h->comm->allreduce_sum_i64(h->rank, gWb, NG * nv, h->st);
+    h->comm->allreduce_max_i32(h->rank, gtau, NG, h->st);
+    CK(cudaMemcpyAsync(hW.data(), gWb, hW.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(htau.data(), gtau, htau.size() * 4, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  } catch (...) {
+    cudaFree(dgid);
+    cudaFree(gWb);
+    cudaFree(gtau);
+    throw;
+  }
+  cudaFree(dgid);
+  cudaFree(gWb);
+  cudaFree(gtau);
+  for (int c = 0; c < NG; ++c) require(htau[c] >= 0, "repartition: a cell is owned by no rank");
+  // 2. the new partition: the caller's, or level-cost slabs
+  std::vector<int32_t> roc(NG);
+  if (roc_in) {
+    for (int c = 0; c < NG; ++c) {
+      require(roc_in[c] >= 0 && roc_in[c] < h->nranks, "repartition: rank_of_cell out of range");
+      roc[c] = roc_in[c];
+    }
+  } else {
+    int theta = 0;
+    for (int c = 0; c < NG; ++c) theta = std::max(theta, htau[c]);
+    std::vector<double> wgt(NG);
+    for (int c = 0; c < NG; ++c) wgt[c] = (double)(1ll << (theta - htau[c]));
+    tafv::partition_slabs(*gm, h->nranks, axis, wgt.data(), roc.data());
+  }
+  if (roc_out) std::memcpy(roc_out, roc.data(), (size_t)NG * 4);
+  // 3. the new shard (host description first: a bad partition leaves the
+  // handle untouched), then the in-place rebuild
+  const tafv::Shard sh = tafv::build_shard(*gm, roc.data(), h->rank, h->nranks);
+  const tafv_mesh_view lv = sh.view(gm->dim);
+  std::vector<double> Wg((size_t)NG * nv);
+  std::memcpy(Wg.data(), hW.data(), Wg.size() * 8);
+  hW.clear();
+  hW.shrink_to_fit();
+  const double t0 = h->t0;
+  const int iteration = h->iteration;
+  tafv_comm* comm = h->comm;
+  const int device = h->device;
+  const tafv_physics phys = h->phys;
+  const bool use_graph = h->use_graph, plan_graph_on = h->plan_graph_on, slot_geo = h->slot_geo,
+             slot_n = h->slot_n, slot_dx = h->slot_dx, face_dx = h->face_dx, alt_dir = h->alt_dir,
+             iwin_alias = h->iwin_alias;
+  const int dl_stream = h->dl_stream, batch_lanes = h->batch_lanes;
+  const tafv_mesh_view* rep_mesh = h->rep_mesh;
+  const int rep_every = h->rep_every, rep_axis = h->rep_axis;
+  h->release();
+  *h = tafv_gpu{};
+  h->use_graph = use_graph;
+  h->plan_graph_on = plan_graph_on;
+  h->slot_geo = slot_geo;
+  h->slot_n = slot_n;
+  h->slot_dx = slot_dx;
+  h->face_dx = face_dx;
+  h->alt_dir = alt_dir;
+  h->iwin_alias = iwin_alias;
+  h->dl_stream = dl_stream;
+  h->batch_lanes = batch_lanes;
+  h->rep_mesh = rep_mesh;
+  h->rep_every = rep_every;
+  h->rep_axis = rep_axis;
+  init_handle(h, &lv, &phys, device, &sh, comm, NG);
+  const int rc = tafv_gpu_set_state(h, nullptr, Wg.data(), t0, iteration);
+  if (rc != TAFV_OK) throw Error{rc, h->err};
+  h->levels_made = true;  // the next plan_iteration rebuilds them; tau is the old map
+  h->rep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+int tafv_gpu_repartition(tafv_gpu* h, const tafv_mesh_view* global_mesh, const int32_t* rank_of_cell,
+                         int32_t axis, int32_t* rank_of_cell_out) {
+  return guard(h, [&] { repartition(h, global_mesh, rank_of_cell, axis, rank_of_cell_out); });
+}
+
+int tafv_gpu_set_repartition(tafv_gpu* h, const tafv_mesh_view* global_mesh, int32_t every, int32_t axis) {
+  return guard(h, [&] {
+    require(every >= 0, "repartition_every must be >= 0");
+    require(every == 0 || h->sharded(), "repartition_every: the handle is not a shard");
+    require(every == 0 || (global_mesh != nullptr && global_mesh->n_cells == h->N_global),
+            "repartition_every: global mesh differs from the shard's");
+    require(axis >= 0 && axis <= 2, "repartition_every: axis must be 0, 1 or 2");
+    h->rep_mesh = every ? global_mesh : nullptr;
+    h->rep_every = every;
+    h->rep_axis = axis;
+  });
+}
+
 int tafv_gpu_iterate(tafv_gpu* h, const tafv_options* opt, int32_t n, tafv_record* out) {
   return guard(h, [&] {
     require(opt != nullptr, "iterate: null options");
     require(n >= 0, "integrate: negative iteration count");
+    if (h->rep_every > 0 && h->sharded()) {
+      // DistDriver::integrate (exchange.cpp:611-618): repartition before
+      // iteration i whenever i > 0 and i % repartition_every == 0
+      int64_t launches = 0;
+      double ms3[3] = {0, 0, 0};
+      for (int i = 0; i < n; i += h->rep_every) {
+        if (i > 0) repartition(h, h->rep_mesh, nullptr, h->rep_axis, nullptr);
+        const int m = std::min<int>(h->rep_every, n - i);
+        timed_call(*h, [&] { integrate_pipelined(*h, *opt, m, out ? out + i : nullptr, true); });
+        launches += h->launches;
+        for (int q = 0; q < 3; ++q) ms3[q] += h->ms[q];
+      }
+      h->launches = launches;
+      for (int q = 0; q < 3; ++q) h->ms[q] = ms3[q];
+      return;
+    }
     timed_call(*h, [&] { integrate_pipelined(*h, *opt, n, out, true); });
   });
 }
@@ -2240,6 +2419,8 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->d_cperm = h.d_cperm;
     t->d_fperm = h.d_fperm;
     t->slot_geo = h.slot_geo;
+    t->slot_n = h.slot_n;
+    t->slot_dx = h.slot_dx;
     t->face_dx = h.face_dx;
     t->iwin_alias = h.iwin_alias;
     t->alt_dir = h.alt_dir;
@@ -2501,6 +2682,7 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     };
     if (n == "w") rows(h->w, h->N, h->nv, h->d_cperm);
     else if (n == "W") rows(h->W, h->N, h->nv, h->d_cperm);
+    else if (n == "repartition_ms") *static_cast<double*>(out) = h->rep_ms;
     else if (n == "w_pred") rows(h->wp, h->N, h->nv, h->d_cperm);
     else if (n == "grad") {  // unpadded rows of nv*3
       const size_t w3 = (size_t)h->nv * 3;
@@ -2587,6 +2769,12 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+      drop_graphs(*h);
+    } else if (n == "slot_n") {
+      h->slot_n = value != 0;
+      drop_graphs(*h);
+    } else if (n == "slot_dx") {
+      h->slot_dx = value != 0;
       drop_graphs(*h);
     } else if (n == "slot_geo") {
       h->slot_geo = value != 0;

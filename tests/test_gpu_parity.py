@@ -9,6 +9,7 @@ proj/tests/test_dist.cpp:394-395 allows) within 1e-12 relative.
 """
 import math
 import os
+import threading
 
 import numpy as np
 import pytest
@@ -710,6 +711,132 @@ def test_sharded_repartition_by_level_cost_bitwise(gpu):
     g.reference_integrate(cfg.options(), n1 + n2)
     np.testing.assert_array_equal(w, g.get_state()[0])
     assert out[0][3] == n1 + n2
+
+
+def _threads(world, body):
+    errs = []
+
+    def wrap(r):
+        try:
+            body(r)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=wrap, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+
+
+@pytest.mark.parametrize("cid,scale,world,axis,explicit", [(3, 10, 2, 0, False), (2, 5, 3, 1, False),
+                                                           (4, 20, 2, 0, True)])
+def test_in_library_repartition_bitwise(cid, scale, world, axis, explicit, gpu):
+    """tafv_gpu_repartition (DistDriver::repartition, exchange.cpp:595-609)
+    in place on `world` loopback ranks: the owned rows and levels are
+    all-reduced on the device, the level-cost slabs (or an explicit
+    partition along another axis) re-cut, the shards rebuilt without the
+    caller re-creating them -- and the continued run equals the single
+    domain bitwise (state, t0, iteration, records)."""
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    cfg = configs.get(cid, scale)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    n1, n2 = 2, 2
+    roc = shard.partition_slabs(mesh, world, axis=axis)
+    comm = Comm.loopback(world)
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(world)]
+    target = shard.partition_slabs(mesh, world, axis=(axis + 1) % 3) if explicit else None
+    out = {}
+
+    def body(r):
+        s = solvers[r]
+        s.set_state(w0)
+        r1 = s.reference_integrate(opt, n1)
+        tau = s.get_array("tau")
+        new = s.repartition(target, axis=axis)
+        r2 = s.reference_integrate(opt, n2)
+        out[r] = (r1 + r2, s.get_state(), new, tau, s.get_array("repartition_ms")[0])
+
+    _threads(world, body)
+    for s in solvers:
+        s.close()
+    comm.close()
+    new = out[0][2]
+    for r in range(world):
+        np.testing.assert_array_equal(out[r][2], new)
+    if explicit:
+        np.testing.assert_array_equal(new, target)
+    else:
+        # the reference's weights: 2^(theta - tau) of the last plan
+        tau = sum(np.where(roc == r, out[r][3], 0) for r in range(world))
+        np.testing.assert_array_equal(new, shard.partition_slabs(mesh, world, axis=axis,
+                                                                 weight=shard.level_cost_weights(tau)))
+    assert not np.array_equal(new, roc)  # the cut moved
+    w = sum(out[r][1][0] * (new == r)[:, None] for r in range(world))
+    W = sum(out[r][1][1] * (new == r)[:, None] for r in range(world))
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    ref = g.reference_integrate(opt, n1 + n2)
+    wr, Wr, t0r, itr = g.get_state()
+    np.testing.assert_array_equal(w, wr)
+    np.testing.assert_array_equal(W, Wr)
+    for r in range(world):
+        recs = out[r][0]
+        assert out[r][1][2:] == (t0r, itr)
+        assert [x["dt"] for x in recs] == [x["dt"] for x in ref]
+        assert [x["level_cells"] for x in recs] == [x["level_cells"] for x in ref]
+        assert out[r][4] > 0.0
+
+
+def test_repartition_every_matches_single_domain(gpu):
+    """DistOptions::repartition_every through reference_integrate
+    (DistDriver::integrate, exchange.cpp:611-618): 5 iterations with a
+    repartition before iterations 2 and 4 equal the single domain bitwise;
+    repartitioning before any plan is the reference's logic_error."""
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm, LogicError
+    cfg = configs.get(3, 10)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    world = 2
+    roc = shard.partition_slabs(mesh, world, axis=0)
+    comm = Comm.loopback(world)
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(world)]
+    out = {}
+
+    def body(r):
+        s = solvers[r]
+        s.set_state(w0)
+        try:
+            s.repartition()
+        except LogicError as e:
+            out[("err", r)] = str(e)
+        s.set_repartition(2, axis=0)
+        recs = s.reference_integrate(opt, 5)
+        out[r] = (recs, s.get_state())
+
+    _threads(world, body)
+    for s in solvers:
+        s.close()
+    comm.close()
+    assert "repartition before any iteration" in out[("err", 0)]
+    g = Solver(mesh, "euler")
+    g.set_state(w0)
+    ref = g.reference_integrate(opt, 5)
+    wr = g.get_state()[0]
+    # each rank's get_state fills the rows it owns now; every row is owned once
+    owned = [np.any(out[r][1][1] != 0.0, axis=1) for r in range(world)]
+    assert np.all(sum(o.astype(int) for o in owned) == 1)
+    w = sum(out[r][1][0] * owned[r][:, None] for r in range(world))
+    np.testing.assert_array_equal(w, wr)
+    for r in range(world):
+        assert [x["dt"] for x in out[r][0]] == [x["dt"] for x in ref]
+        assert [x["level_cells"] for x in out[r][0]] == [x["level_cells"] for x in ref]
 
 
 def test_raw_levels_and_dt_max_arrays(gpu):

@@ -22,8 +22,10 @@ def _ngpus():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nproc,config,scale", [(2, 2, 2), (0, 3, 4)])
-def test_nccl_shards_bitwise(nproc, config, scale, tmp_path):
+@pytest.mark.parametrize("nproc,config,scale,rep", [(2, 2, 2, 0), (0, 3, 4, 0), (2, 3, 10, 1)])
+def test_nccl_shards_bitwise(nproc, config, scale, rep, tmp_path):
+    """rep > 0: in-library repartition (tafv_gpu_repartition, state migrated
+    by NCCL all-reduces) before every rep-th iteration."""
     n = _ngpus()
     if n < 2:
         pytest.skip(f"needs >= 2 GPUs (found {n})")
@@ -31,7 +33,7 @@ def test_nccl_shards_bitwise(nproc, config, scale, tmp_path):
     out = tmp_path / "verdict.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", "--master-port=29517", os.path.join(ROOT, "tools", "multigpu_worker.py"),
-           "--config", str(config), "--scale", str(scale), "--iters", "3", "--out", str(out)]
+           "--config", str(config), "--scale", str(scale), "--iters", "3", "--repartition-every", str(rep), "--out", str(out)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads(out.read_text())

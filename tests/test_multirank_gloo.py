@@ -55,7 +55,7 @@ def _allreduce(x, op):
     return float(t.item())
 
 
-def _rank_main(rank, world, port, cid, scale, iters, out):
+def _rank_main(rank, world, port, cid, scale, iters, out, rep_every=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -64,21 +64,49 @@ def _rank_main(rank, world, port, cid, scale, iters, out):
     cfg = configs.periodic_blast() if cid == "P" else configs.get(cid, scale)
     mesh = cfg.mesh()
     w0 = cfg.initial_state(mesh)
-    roc = shard.partition_slabs(mesh, world, axis=0)
-    sh = shard.describe(mesh, roc, rank, world)
-    lm = shard.local_mesh(mesh, sh)
-    cls = sh["cls"]
-    own = np.flatnonzero(cls == 0).astype(np.int32)
-    o = OracleSolver(OracleMesh(lm, closure_mask=cls <= 1), "euler")
-    o.init_values(w0[sh["cells"]].reshape(-1))
     opt = cfg.options()
-    nloc = len(sh["cells"])
-    fl, fr = lm["fl"], lm["fr"]
-    inner = fr >= 0
-    touch_own = (cls[fl] == 0) | (inner & (cls[np.maximum(fr, 0)] == 0))
     nv = 5
+    NG = len(mesh["vol"])
+
+    def build(roc, w_global=None, W_global=None):
+        sh = shard.describe(mesh, roc, rank, world)
+        lm = shard.local_mesh(mesh, sh)
+        cls = sh["cls"]
+        own = np.flatnonzero(cls == 0).astype(np.int32)
+        o = OracleSolver(OracleMesh(lm, closure_mask=cls <= 1), "euler")
+        if W_global is None:
+            o.init_values(w_global[sh["cells"]].reshape(-1))
+        else:  # a repartition: the committed W carries over, w = W / V (intensive_correct)
+            Wl = W_global[sh["cells"]]
+            o.init_values((Wl / lm["vol"][:, None]).reshape(-1))
+            o.set("W", Wl.reshape(-1))
+            o.set("w", (Wl / lm["vol"][:, None]).reshape(-1))
+        return sh, lm, cls, own, o
+
+    roc = shard.partition_slabs(mesh, world, axis=0)
+    sh, lm, cls, own, o = build(roc, w_global=w0)
     totals = []
+    tau = None
     for it in range(iters):
+        if rep_every and it > 0 and it % rep_every == 0:
+            # DistDriver::repartition (exchange.cpp:595-609) as the library
+            # does it (tafv_gpu_repartition): owned W rows as bit patterns and
+            # the last plan's levels all-reduced, level-cost slabs re-cut
+            Wb = np.zeros((NG, nv), dtype=np.int64)
+            Wb[sh["cells"][own]] = o.get("W").reshape(-1, nv)[own].view(np.int64)
+            tg = np.full(NG, -1, dtype=np.int32)
+            tg[sh["cells"][own]] = tau[own]
+            Wt, tt = torch.from_numpy(Wb), torch.from_numpy(tg)
+            dist.all_reduce(Wt, op=dist.ReduceOp.SUM)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tg = tt.numpy()
+            assert (tg >= 0).all()
+            roc = shard.partition_slabs(mesh, world, axis=0, weight=shard.level_cost_weights(tg))
+            sh, lm, cls, own, o = build(roc, W_global=Wt.numpy().view(np.float64))
+        nloc = len(sh["cells"])
+        fl, fr = lm["fl"], lm["fr"]
+        inner = fr >= 0
+        touch_own = (cls[fl] == 0) | (inner & (cls[np.maximum(fr, 0)] == 0))
         # ---- plan (reference.cpp:89-98, distributed) ----
         o.kernel("compute_dt_max", own, cfl=opt.cfl, dt_cap=opt.dt_cap)
         dt = _allreduce(o.kernel("min_dt", own), dist.ReduceOp.MIN)
@@ -151,17 +179,20 @@ def _rank_main(rank, world, port, cid, scale, iters, out):
     dist.destroy_process_group()
 
 
-def _run(world, cid, scale, iters):
+def _run(world, cid, scale, iters, rep_every=0):
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_rank_main, args=(world, port, cid, scale, iters, out), nprocs=world,
+    mp.start_processes(_rank_main, args=(world, port, cid, scale, iters, out, rep_every), nprocs=world,
                        join=True, start_method="fork")
     return dict(out)
 
 
-@pytest.mark.parametrize("world,cid,scale,iters", [(2, 2, 5, 3), (3, 3, 10, 2), (2, 4, 20, 2), (2, "P", 1, 3)])
-def test_decomposed_run_matches_single_domain_bitwise(world, cid, scale, iters):
+@pytest.mark.parametrize("world,cid,scale,iters,rep_every", [(2, 2, 5, 3, 0), (3, 3, 10, 2, 0), (2, 4, 20, 2, 0),
+                                                             (2, "P", 1, 3, 0), (2, 3, 10, 3, 2), (3, 2, 5, 3, 1)])
+def test_decomposed_run_matches_single_domain_bitwise(world, cid, scale, iters, rep_every):
+    """rep_every > 0: level-cost repartitions in between (state migrated by
+    all-reduces of the owned rows' bit patterns, as tafv_gpu_repartition)."""
     from oracle import OracleSolver
     from paper_1704_01144_b200 import configs
     cfg = configs.periodic_blast() if cid == "P" else configs.get(cid, scale)
@@ -172,7 +203,7 @@ def test_decomposed_run_matches_single_domain_bitwise(world, cid, scale, iters):
     opt = cfg.options()
     ref.set_options(opt.theta_max, opt.cfl, opt.dt_cap)
     recs = ref.integrate(iters)
-    res = _run(world, cid, scale, iters)
+    res = _run(world, cid, scale, iters, rep_every)
     w = np.full((len(mesh["vol"]), 5), np.nan)
     W = np.full((len(mesh["vol"]), 5), np.nan)
     for r in range(world):

@@ -6,7 +6,8 @@ inside (NCCL send/recv on the priority comm stream), `--iters` iterations.
 Rank 0 then runs the single-domain solver on its GPU and checks bitwise
 equality of the assembled owned rows (w, W) and of every record's dt,
 level counts and cost ratio, plus the ledger totals within 1e-12. Writes a
-JSON verdict to --out."""
+JSON verdict to --out. --repartition-every k re-cuts the slabs in the library
+(tafv_gpu_repartition over NCCL) before every k-th iteration."""
 import argparse
 import json
 import os
@@ -26,6 +27,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--scale", type=int, default=2)
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--repartition-every", type=int, default=0,
+                help="DistOptions::repartition_every: in-library level-cost repartition (NCCL state migration)")
 ap.add_argument("--out", required=True)
 a = ap.parse_args()
 
@@ -42,6 +45,8 @@ dist.broadcast_object_list(uid, src=0)
 comm = Comm.nccl(uid[0], rank, world, device=local)
 s = Solver(mesh, "euler", device=local, shard=(roc, rank, comm))
 s.set_state(w0)
+if a.repartition_every:
+    s.set_repartition(a.repartition_every, axis=0)
 recs = s.reference_integrate(opt, a.iters)
 w, W, t0, it = s.get_state()  # owned rows, zeros elsewhere
 pair = torch.from_numpy(np.stack([w, W])).cuda()

@@ -44,22 +44,61 @@ def short(name):
     return name.replace("void ", "").replace("tafv::", "").split("(")[0]
 
 
-def launches(tag):
-    rows = [r for r in csv.reader(open(os.path.join(OUT, f"launches_{tag}.csv"))) if len(r) > 5]
+def launch_rows(tag):
+    """{launch id: {"name", metric: value in base units}} from a launch list
+    (one or several metrics per launch; ncu's preamble lines skipped)."""
+    lines = open(os.path.join(OUT, f"launches_{tag}.csv")).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.reader(lines[start:]))
     hdr = rows[0]
-    i_n, i_v = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    agg = collections.OrderedDict()
+    ix = {h: i for i, h in enumerate(hdr)}
+    per = collections.OrderedDict()
     for r in rows[1:]:
-        agg.setdefault(short(r[i_n]), []).append(float(r[i_v].replace(",", "")) / 1e3)
-    tot = sum(sum(v) for v in agg.values())
-    lines = [f"# {tag}: ncu launch list of `python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1`",
-             "", "`ncu --metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised",
-             "launches: compare SHARES with bench.py's event-timed breakdown, not absolutes).", "",
-             "| kernel | launches | total us | share of kernel time | avg us |", "|---|---|---|---|---|"]
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v) / tot * 100:.1f} % | {sum(v) / len(v):.1f} |")
-    lines.append(f"| **all** | {sum(len(v) for v in agg.values())} | {tot:.1f} | 100 % | |")
+        if len(r) != len(hdr):
+            continue
+        d = per.setdefault(r[ix["ID"]], {"name": short(r[ix["Kernel Name"]])})
+        d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", "")) * UNIT.get(r[ix["Metric Unit"]], 1.0)
+    return per
+
+
+def launches(tag, what):
+    per = launch_rows(tag)
+    agg = collections.OrderedDict()
+    for d in per.values():
+        a = agg.setdefault(d["name"], [0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += d.get("gpu__time_duration.sum", 0.0) / 1e3
+        a[2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    tot = sum(v[1] for v in agg.values())
+    dram = any(v[2] for v in agg.values())
+    lines = [f"# {tag}: ncu launch list of `{what}`",
+             "", "`ncu --metrics gpu__time_duration.sum[,dram__bytes_read.sum,dram__bytes_write.sum] --clock-control none`",
+             "(cold-cache, serialised launches: compare SHARES with bench.py's event-timed breakdown, not absolutes).", "",
+             "| kernel | launches | total us | share of kernel time | avg us |" + (" DRAM GB | DRAM TB/s |" if dram else ""),
+             "|---|---|---|---|---|" + ("---|---|" if dram else "")]
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        row = f"| `{k}` | {v[0]} | {v[1]:.1f} | {v[1] / tot * 100:.1f} % | {v[1] / v[0]:.1f} |"
+        if dram:
+            row += f" {v[2] / 1e9:.2f} | {v[2] / max(v[1], 1e-9) / 1e6:.2f} |"
+        lines.append(row)
+    lines.append(f"| **all** | {sum(v[0] for v in agg.values())} | {tot:.1f} | 100 % | |" + (" | |" if dram else ""))
     return "\n".join(lines) + "\n"
+
+
+def launch_traffic(tag):
+    """Mean DRAM bytes per launch of each bench kernel kind over the launch
+    list (every launch of the profiled iteration), when it carries DRAM bytes."""
+    per = launch_rows(tag)
+    tr = {}
+    for d in per.values():
+        if "dram__bytes_read.sum" not in d:
+            return {}
+        kind = kind_of(d["name"])
+        if kind:
+            tr.setdefault(kind, []).append(d["dram__bytes_read.sum"] + d.get("dram__bytes_write.sum", 0.0))
+    return {k: {"bytes_per_launch": sum(v) / len(v), "launches": len(v),
+                "source": f"profiles/{tag}_launches.md (ncu launch list, cold cache, mean over every launch of the "
+                          "profiled iteration)"} for k, v in tr.items()}
 
 
 METRICS = [  # (metric, column, scale from base units: ns / bytes)
@@ -96,14 +135,13 @@ def val(r, hdr, units, m):
 
 
 def full(tag):
-    lines = [f"# {tag}: ncu --set full, one iteration's worth of launches per hot kernel", "",
-             "`ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 40 -c 8` on",
-             "the same bench command (cache flushed between replays: cold-cache numbers).", ""]
+    lines = [f"# {tag}: ncu --set full captures (gpurun_out/full_{tag}*.ncu-rep)", "",
+             "`ncu --set full --clock-control none --import-source on -k regex:<kernels> [-c N]` on the",
+             "profiled command of the launch list (cache flushed between replays: cold-cache numbers).", ""]
     traffic = {}
-    for k in ("k_grad_limit", "k_face_flux", "k_gather_update"):
-        rep = os.path.join(OUT, f"full_{tag}_{k}.ncu-rep")
-        if not os.path.exists(rep):
-            continue
+    import glob
+    for rep in sorted(glob.glob(os.path.join(OUT, f"full_{tag}*.ncu-rep"))):
+        k = os.path.basename(rep)[len(f"full_{tag}"):-len(".ncu-rep")].strip("_") or tag
         hdr, units, rows = raw_rows(rep)
         lines += [f"## `{k}`", "", "| launch | kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls (cycles/issue) |",
                   "|---" * (len(METRICS) + 3) + "|"]
@@ -132,10 +170,12 @@ def full(tag):
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+    what = sys.argv[2] if len(sys.argv) > 2 else "python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 1"
     os.makedirs(PROF, exist_ok=True)
-    open(os.path.join(PROF, f"{tag}_launches.md"), "w").write(launches(tag))
+    open(os.path.join(PROF, f"{tag}_launches.md"), "w").write(launches(tag, what))
     md, tj = full(tag)
     open(os.path.join(PROF, f"{tag}_kernels.md"), "w").write(md)
+    tj.update(launch_traffic(tag))  # every launch of the iteration beats a sample of launches
     json.dump(tj, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
     print(json.dumps(tj, indent=1))
 
