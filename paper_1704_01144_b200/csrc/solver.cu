@@ -2619,7 +2619,9 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
     require(n >= 0, "integrate: negative iteration count");
     batch_setup(*h, *opt, 0, false);
     const size_t total = (size_t)h->N * h->nv;
-    const size_t chunk = std::max<size_t>(1, std::min<size_t>(total, (size_t)8 << 20));  // 64 MB
+    size_t chunk_mb = 64;
+    if (const char* e = getenv("TAFV_E2E_CHUNK_MB")) chunk_mb = std::max(1, atoi(e));  // A/B
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(total, (chunk_mb << 20) / sizeof(double)));
     const int nchunks = (int)((total + chunk - 1) / chunk);
     while ((int)h->ev_chunk.size() < nchunks) {
       cudaEvent_t e;
@@ -2630,8 +2632,28 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
     const int grid = h->grid_for((long long)total, 256);
     h->ms[0] = h->ms[1] = h->ms[2] = 0.0;
     h->launches = 0;
+    // TAFV_E2E_TRACE: per-iteration stage times on stderr (upload, load,
+    // plan + sweep, scatter, download), from events on the stages' streams
+    const char* trace_env = getenv("TAFV_E2E_TRACE");
+    const bool trace = trace_env != nullptr && atoi(trace_env) == 1;
+    // TAFV_E2E_TRACE=2: an unsynchronised timeline (event per stage boundary
+    // per iteration, printed at the end relative to the first)
+    const bool tline = trace_env != nullptr && atoi(trace_env) == 2;
+    std::vector<std::pair<const char*, cudaEvent_t>> tl;
+    auto mark = [&](const char* what, cudaStream_t q) {
+      if (!tline) return;
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      CK(cudaEventRecord(e, q));
+      tl.emplace_back(what, e);
+    };
+    cudaEvent_t tev[6] = {};
+    if (trace)
+      for (auto& e : tev) CK(cudaEventCreate(&e));
     try {
       for (int it = 0; it < n; ++it) {
+        mark("upload start", h->cin);
+        if (trace) CK(cudaEventRecord(tev[0], h->cin));
         for (int c = 0; c < nchunks; ++c) {  // upload chunk c once its previous download landed
           const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
           CK(cudaStreamWaitEvent(h->cin, h->ev_chunk[c], 0));
@@ -2639,24 +2661,52 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
         }
         CK(cudaEventRecord(h->ev_in[0], h->cin));
         CK(cudaStreamWaitEvent(h->st, h->ev_in[0], 0));
+        mark("uploads done", h->cin);
+        if (trace) CK(cudaEventRecord(tev[1], h->st));
         k_load_extensive<<<grid, 256, 0, h->st>>>(h->bin[0], h->d_cperm, h->vol, h->N, h->nv, h->W, h->w);
         CK(cudaGetLastError());
+        if (trace) CK(cudaEventRecord(tev[2], h->st));
         h->state_set = true;
         h->has_plan = false;
         const int64_t l0 = h->launches;
         double ms0[3] = {h->ms[0], h->ms[1], h->ms[2]};
+        mark("load done", h->st);
         timed_call(*h, [&] { integrate_pipelined(*h, *opt, 1, out ? out + it : nullptr, true); });
         for (int q = 0; q < 3; ++q) h->ms[q] += ms0[q];
         h->launches += l0;
+        mark("sweep done", h->st);
+        if (trace) CK(cudaEventRecord(tev[3], h->st));
         k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[0]);
         CK(cudaGetLastError());
         CK(cudaEventRecord(h->ev_out[0], h->st));
         CK(cudaStreamWaitEvent(h->cout, h->ev_out[0], 0));
+        if (trace) CK(cudaEventRecord(tev[4], h->cout));
+        mark("scatter done / downloads start", h->cout);
         for (int c = 0; c < nchunks; ++c) {
           const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
           CK(cudaMemcpyAsync(W_host + a, h->bout[0] + a, len * sizeof(double), cudaMemcpyDeviceToHost, h->cout));
           CK(cudaEventRecord(h->ev_chunk[c], h->cout));
         }
+        mark("downloads done", h->cout);
+        if (trace) {
+          CK(cudaEventRecord(tev[5], h->cout));
+          CK(cudaEventSynchronize(tev[5]));
+          float d[5];
+          for (int q = 0; q < 5; ++q) CK(cudaEventElapsedTime(&d[q], tev[q], tev[q + 1]));
+          fprintf(stderr, "E2E it %d upload %.2f load %.2f plan+sweep %.2f scatter %.2f download %.2f ms\n", it,
+                  d[0], d[1], d[2], d[3], d[4]);
+        }
+      }
+      if (trace)
+        for (auto& e : tev) cudaEventDestroy(e);
+      if (tline) {
+        CK(cudaStreamSynchronize(h->cout));
+        for (auto& m : tl) {
+          float t = 0.f;
+          CK(cudaEventElapsedTime(&t, tl[0].second, m.second));
+          fprintf(stderr, "E2E %9.2f ms  %s\n", t, m.first);
+        }
+        for (auto& m : tl) cudaEventDestroy(m.second);
       }
       CK(cudaStreamSynchronize(h->cout));
     } catch (...) {
