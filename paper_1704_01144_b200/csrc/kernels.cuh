@@ -238,6 +238,30 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
 #endif
 }
 
+// ---- bulk copies into shared memory (TMA engine, mbarrier completion) ------
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// One elected thread: expect `bytes` on the barrier and start the copy.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of dst before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- K1: stage + Green-Gauss + Barth-Jespersen ----------------------------
 // Thread per cell, all NV components in registers (measured faster than a
 // component-parallel layout, which multiplies the shared index/geometry
@@ -245,6 +269,12 @@ __device__ __forceinline__ double bj_update(double alpha, double delta, double h
 // by slot in CSR order. DEG = 6 is the hex fast path (implicit offsets, fully
 // unrolled slot loop); DEG = 0 reads the CSR offsets. The active count comes
 // from device memory so the launch is graph-capturable.
+#ifndef TAFV_K1_TILE
+#define TAFV_K1_TILE 1  // identity phases: Morton-brick staging in shared memory
+#endif
+#ifndef TAFV_K1_TILE_SDX
+#define TAFV_K1_TILE_SDX 0  // with TILE: the brick's limiter offsets by one bulk copy (A/B)
+#endif
 #ifndef TAFV_K1_MINB
 #define TAFV_K1_MINB 5  // min resident 128-thread blocks/SM for K1 (register cap 102; measured best)
 #endif
@@ -256,13 +286,12 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
   constexpr int NV = P::NV, D = P::DIM;
   const int n = *n_dev;
   const int stride = gridDim.x * blockDim.x;
-  for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
-    // rev: walk the items backwards, so this kernel starts on the rows its
-    // predecessor wrote last (still in L2); consecutive kernels alternate.
-    const int i = rev ? n - 1 - ii : ii;
-    const int c = list ? list[i] : base + i;
-    double we[NV];
-    stage_spec<NV>(s, c, front, pred, we);
+  // One active cell c with its staged row we: Green-Gauss + Barth-Jespersen.
+  // Neighbours in [lo, hi) were staged into srow by their own threads.
+  // sdx_tile (tile path): the brick's limiter offsets, bulk-copied into
+  // shared memory at the brick's start (complete when `bar` flips `parity`)
+  auto cell = [&](int c, const double* we, int lo, int hi, const double* srow, const double4* sdx_tile,
+                  uint64_t* bar, unsigned parity) {
     double g[NV][D];
     double wmin[NV], wmax[NV];
 #pragma unroll
@@ -298,7 +327,12 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #ifdef TAFV_EXP_NO_GATHER
         for (int k = 0; k < NV; ++k) wn[k] = we[k] * (1.0 + 1e-3 * t);  // timing experiment only
 #else
-        stage_spec<NV>(s, nb, front, pred, wn);
+        if (nb >= lo && nb < hi) {  // staged by its own thread in this tile
+#pragma unroll
+          for (int k = 0; k < NV; ++k) wn[k] = srow[(nb - lo) * NV + k];
+        } else {
+          stage_spec<NV>(s, nb, front, pred, wn);
+        }
 #endif
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
@@ -337,6 +371,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
         wmax[k] = wmax[k] - we[k];     // hp: headroom above
         wmin[k] = -(wmin[k] - we[k]);  // hn: headroom below, negated (exact)
       }
+      if (DEG == 6 && sdx_tile) mbar_wait(bar, parity);
 #pragma unroll
       for (int t = s0; t < s1; ++t) {
         double dx0, dx1, dx2;
@@ -344,7 +379,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #ifdef TAFV_EXP_NO_SDX
           const double4 d = make_double4(1e-3 * (t & 15), 1e-3, -1e-3, 0.0);  // timing experiment only
 #else
-          const double4 d = ld4(m.sdx + t);
+          const double4 d = sdx_tile ? sdx_tile[(size_t)DEG * (c - lo) + (t - s0)] : ld4(m.sdx + t);
 #endif
           dx0 = d.x;
           dx1 = d.y;
@@ -381,6 +416,62 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
     double* go = s.grad + (size_t)c * GS;
 #pragma unroll
     for (int q = 0; q < GS; q += 4) st4(go + q, row[q], row[q + 1], row[q + 2], row[q + 3]);
+  };
+#if TAFV_K1_TILE
+  if (DEG == 6 && list == nullptr) {
+    // Identity phase (every cell of [base, base + n) active): a block takes
+    // 128 consecutive cells (a Morton brick), each thread stages its own cell
+    // into shared memory once, and the neighbours inside the brick (~80 % of
+    // the slots) read it there instead of re-staging it from global memory.
+    __shared__ double srow[128 * NV];
+#if TAFV_K1_TILE_SDX
+    // and the brick's limiter offsets arrive by one bulk copy per brick
+    // (cp.async.bulk, TMA engine) while the gradient loop runs
+    __shared__ __align__(128) double4 sdx_tile[128 * 6];
+    __shared__ __align__(8) uint64_t bar;
+    if (threadIdx.x == 0 && m.sdx) mbar_init(&bar, 1);
+    __syncthreads();
+    unsigned parity = 0;
+#endif
+    for (int t0 = blockIdx.x * blockDim.x; t0 < n; t0 += stride) {
+      const int cnt = min((int)blockDim.x, n - t0);
+      // rev: walk the items backwards (see below); the tile is contiguous either way
+      const int lo = base + (rev ? n - t0 - cnt : t0), hi = lo + cnt;
+#if TAFV_K1_TILE_SDX
+      if (threadIdx.x == 0 && m.sdx)
+        bulk_g2s(sdx_tile, m.sdx + (size_t)DEG * lo, (unsigned)(cnt * DEG * sizeof(double4)), &bar);
+#endif
+      const int ii = t0 + threadIdx.x;
+      int c = -1;
+      double we[NV];
+      if (ii < n) {
+        c = base + (rev ? n - 1 - ii : ii);
+        stage_spec<NV>(s, c, front, pred, we);
+#pragma unroll
+        for (int k = 0; k < NV; ++k) srow[(c - lo) * NV + k] = we[k];
+      }
+      __syncthreads();
+#if TAFV_K1_TILE_SDX
+      if (c >= 0) cell(c, we, lo, hi, srow, m.sdx ? sdx_tile : nullptr, &bar, parity);
+      parity ^= 1u;
+#else
+      if (c >= 0) cell(c, we, lo, hi, srow, nullptr, nullptr, 0);
+#endif
+      // the next brick overwrites srow (a second buffer without this barrier
+      // measured slower: the barrier keeps the block's warps on one brick)
+      __syncthreads();
+    }
+    return;
+  }
+#endif
+  for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+    // rev: walk the items backwards, so this kernel starts on the rows its
+    // predecessor wrote last (still in L2); consecutive kernels alternate.
+    const int i = rev ? n - 1 - ii : ii;
+    const int c = list ? list[i] : base + i;
+    double we[NV];
+    stage_spec<NV>(s, c, front, pred, we);
+    cell(c, we, 0, 0, nullptr, nullptr, nullptr, 0);
   }
 }
 
