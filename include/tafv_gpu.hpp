@@ -133,4 +133,65 @@ inline std::vector<IterationRecord> reference_integrate(Solver& s, const SolverO
   return out;
 }
 
+// DistOptions (exchange.hpp:136-144): the options the GPU shards honour.
+struct DistOptions {
+  int repartition_every = 0;  // 0 = keep the initial partition (exchange.hpp:140-142)
+  int axis = 0;               // slab axis of the level-cost re-cuts
+};
+
+// One rank of the distributed integrator (DistDriver, exchange.hpp:149-170,
+// exchange.cpp:541-660): the rank's shard (owned cells + 2-ring halo) of the
+// GLOBAL mesh resident on `device`, the communicator for the collectives and
+// the halo exchange. The caller keeps `mesh` alive (DistDriver keeps its
+// `const Mesh&`). State arrays are GLOBAL: set_state takes the whole state,
+// get_state writes this rank's owned rows. Every call is collective.
+class DistDriver {
+ public:
+  DistDriver(const tafv_mesh_view& mesh, const tafv_physics& physics, std::vector<int32_t> rank_of_cell,
+             int rank, tafv_comm* comm, DistOptions opt = {}, int device = 0)
+      : mesh_(mesh), part_(std::move(rank_of_cell)) {
+    const int rc = tafv_gpu_create_shard(&mesh_, &physics, device, part_.data(), rank, comm, &h_);
+    if (rc != TAFV_OK) throw_status(rc, tafv_gpu_last_error(nullptr));
+    check(tafv_gpu_set_repartition(h_, &mesh_, opt.repartition_every, opt.axis));
+  }
+  ~DistDriver() { tafv_gpu_destroy(h_); }
+  DistDriver(const DistDriver&) = delete;
+  DistDriver& operator=(const DistDriver&) = delete;
+
+  void set_state(const double* w, const double* W = nullptr, double t0 = 0.0, int iteration = 0) {
+    check(tafv_gpu_set_state(h_, w, W, t0, iteration));
+  }
+  void get_state(double* w, double* W, double* t0 = nullptr, int* iteration = nullptr) {
+    int32_t it = 0;
+    check(tafv_gpu_get_state(h_, w, W, t0, &it));
+    if (iteration) *iteration = it;
+  }
+  // DistDriver::integrate (exchange.cpp:611-631), repartition_every included.
+  std::vector<IterationRecord> integrate(const SolverOptions& opt, int iterations) {
+    if (iterations < 0) throw std::invalid_argument("integrate: negative iteration count");
+    std::vector<tafv_record> raw(iterations > 0 ? iterations : 1);
+    const tafv_options o = opt.c();
+    check(tafv_gpu_iterate(h_, &o, iterations, raw.data()));
+    std::vector<IterationRecord> out;
+    for (int i = 0; i < iterations; ++i) out.push_back(to_record(raw[i]));
+    return out;
+  }
+  // DistDriver::repartition (exchange.cpp:595-609): level-cost slabs along
+  // `axis` from the last plan, or the given partition.
+  const std::vector<int32_t>& repartition(int axis = 0, const std::vector<int32_t>* rank_of_cell = nullptr) {
+    check(tafv_gpu_repartition(h_, &mesh_, rank_of_cell ? rank_of_cell->data() : nullptr, axis, part_.data()));
+    return part_;
+  }
+  const std::vector<int32_t>& partition() const { return part_; }
+  tafv_gpu* handle() { return h_; }
+  void check(int rc) const {
+    if (rc != TAFV_OK) throw_status(rc, tafv_gpu_last_error(h_));
+  }
+
+ private:
+  tafv_mesh_view mesh_;
+  std::vector<int32_t> part_;
+  tafv_gpu* h_ = nullptr;
+};
+
 }  // namespace tafv::gpu

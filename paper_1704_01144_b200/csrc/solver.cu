@@ -172,6 +172,8 @@ struct tafv_gpu {
   bool owns_mesh = true;
   int batch_lanes = 2;
   int *d_cperm = nullptr, *d_fperm = nullptr;
+  int* d_cinv = nullptr;  // original -> internal cell (iterate_host's chunked copies; lazily built)
+  std::vector<cudaEvent_t> ev_gather;  // iterate_host: per-chunk "gathered for download" events
   // device state
   double *w = nullptr, *W = nullptr, *wp = nullptr, *grad = nullptr;
   size_t gs = 0;  // gradient row stride in doubles (padded, see GradRow)
@@ -332,7 +334,7 @@ struct tafv_gpu {
     void* ptrs[] = {w,     W,        wp,       bsum,  lpart,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
-                    stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf,
+                    stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf, d_cinv,
                     klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, filist, fblist, fi_counts,
                     fb_counts};
     for (void* p : ptrs)
@@ -350,6 +352,7 @@ struct tafv_gpu {
       if (e) cudaEventDestroy(e);
     for (auto& e : evpool) cudaEventDestroy(e);
     for (auto& e : ev_chunk) cudaEventDestroy(e);
+    for (auto& e : ev_gather) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
     if (cst) cudaStreamDestroy(cst);
     if (lst) cudaStreamDestroy(lst);
@@ -1287,7 +1290,8 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   int tiles = 0;
   for (int q = 0; q < jobs.njobs; ++q) tiles += jobs.j[q].ntiles;
   k_tile_scan<<<jobs.njobs, 1024, 0, h.st>>>(jobs, nkeys, h.dplan, k1 ? 0 : 1);
-  k_tile_scatter<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
+  if (nkeys <= 5) k_tile_scatter_packed<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
+  else k_tile_scatter<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
   h.launches += 3;
   if (h.sharded()) h.comm->allreduce_sum_i64(h.rank, &h.dplan->gcell_count[0], kMaxLevels, h.st);
   CK(cudaGetLastError());
@@ -1425,16 +1429,16 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
       uint8_t* clr = first ? h.fflag : nullptr;
       if (first && last)
         k_level_sweep<true, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
       else if (first)
         k_level_sweep<true, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
       else if (last)
         k_level_sweep<false, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
       else
         k_level_sweep<false, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
       ++h.launches;
       src = dst;
     }
@@ -2621,7 +2625,10 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
     const size_t total = (size_t)h->N * h->nv;
     size_t chunk_mb = 64;
     if (const char* e = getenv("TAFV_E2E_CHUNK_MB")) chunk_mb = std::max(1, atoi(e));  // A/B
-    const size_t chunk = std::max<size_t>(1, std::min<size_t>(total, (chunk_mb << 20) / sizeof(double)));
+    // whole rows per chunk: each chunk is loaded / gathered on its own,
+    // overlapped with the neighbouring chunks' copies
+    const size_t crow = std::max<size_t>(1, (chunk_mb << 20) / (sizeof(double) * h->nv));
+    const size_t chunk = std::min<size_t>(total, crow * h->nv);
     const int nchunks = (int)((total + chunk - 1) / chunk);
     while ((int)h->ev_chunk.size() < nchunks) {
       cudaEvent_t e;
@@ -2629,7 +2636,17 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
       CK(cudaEventRecord(e, h->cout));  // initially complete
       h->ev_chunk.push_back(e);
     }
-    const int grid = h->grid_for((long long)total, 256);
+    while ((int)h->ev_gather.size() < nchunks) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->ev_gather.push_back(e);
+    }
+    if (!h->d_cinv) {
+      h->d_cinv = dalloc<int>(std::max(1, h->N));
+      prep::k_invert<<<h->grid_for(h->N, 256), 256, 0, h->st>>>(h->d_cperm, h->N, h->d_cinv);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(h->st));
+    }
     h->ms[0] = h->ms[1] = h->ms[2] = 0.0;
     h->launches = 0;
     // TAFV_E2E_TRACE: per-iteration stage times on stderr (upload, load,
@@ -2654,36 +2671,45 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
       for (int it = 0; it < n; ++it) {
         mark("upload start", h->cin);
         if (trace) CK(cudaEventRecord(tev[0], h->cin));
-        for (int c = 0; c < nchunks; ++c) {  // upload chunk c once its previous download landed
+        for (int c = 0; c < nchunks; ++c) {
+          // upload chunk c once its previous download landed (which also
+          // means its rows were gathered, so they may be overwritten), then
+          // load it (W, w = W / V) behind the copy while chunk c + 1 uploads
           const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
           CK(cudaStreamWaitEvent(h->cin, h->ev_chunk[c], 0));
           CK(cudaMemcpyAsync(h->bin[0] + a, W_host + a, len * sizeof(double), cudaMemcpyHostToDevice, h->cin));
+          CK(cudaEventRecord(h->ev_gather[c], h->cin));  // (reused: chunk c landed)
+          CK(cudaStreamWaitEvent(h->st, h->ev_gather[c], 0));
+          k_load_extensive_chunk<<<h->grid_for((long long)len, 256), 256, 0, h->st>>>(
+              h->bin[0] + a, h->d_cinv, h->vol, (long long)(a / h->nv), (long long)(len / h->nv), h->nv, h->W, h->w);
+          CK(cudaGetLastError());
         }
-        CK(cudaEventRecord(h->ev_in[0], h->cin));
-        CK(cudaStreamWaitEvent(h->st, h->ev_in[0], 0));
         mark("uploads done", h->cin);
+        mark("loads done", h->st);
         if (trace) CK(cudaEventRecord(tev[1], h->st));
-        k_load_extensive<<<grid, 256, 0, h->st>>>(h->bin[0], h->d_cperm, h->vol, h->N, h->nv, h->W, h->w);
-        CK(cudaGetLastError());
         if (trace) CK(cudaEventRecord(tev[2], h->st));
         h->state_set = true;
         h->has_plan = false;
         const int64_t l0 = h->launches;
         double ms0[3] = {h->ms[0], h->ms[1], h->ms[2]};
-        mark("load done", h->st);
         timed_call(*h, [&] { integrate_pipelined(*h, *opt, 1, out ? out + it : nullptr, true); });
         for (int q = 0; q < 3; ++q) h->ms[q] += ms0[q];
         h->launches += l0;
         mark("sweep done", h->st);
         if (trace) CK(cudaEventRecord(tev[3], h->st));
-        k_scatter_rows<<<grid, 256, 0, h->st>>>(h->W, h->d_cperm, h->N, h->nv, h->bout[0]);
-        CK(cudaGetLastError());
-        CK(cudaEventRecord(h->ev_out[0], h->st));
-        CK(cudaStreamWaitEvent(h->cout, h->ev_out[0], 0));
-        if (trace) CK(cudaEventRecord(tev[4], h->cout));
-        mark("scatter done / downloads start", h->cout);
+        // gather chunk c into original order on the library stream and
+        // download it on the copy stream while chunk c + 1 is gathered
         for (int c = 0; c < nchunks; ++c) {
           const size_t a = (size_t)c * chunk, len = std::min(chunk, total - a);
+          k_gather_orig_chunk<<<h->grid_for((long long)len, 256), 256, 0, h->st>>>(
+              h->W, h->d_cinv, (long long)(a / h->nv), (long long)(len / h->nv), h->nv, h->bout[0] + a);
+          CK(cudaGetLastError());
+          CK(cudaEventRecord(h->ev_gather[c], h->st));
+          CK(cudaStreamWaitEvent(h->cout, h->ev_gather[c], 0));
+          if (c == 0) {
+            if (trace) CK(cudaEventRecord(tev[4], h->cout));
+            mark("first chunk gathered / downloads start", h->cout);
+          }
           CK(cudaMemcpyAsync(W_host + a, h->bout[0] + a, len * sizeof(double), cudaMemcpyDeviceToHost, h->cout));
           CK(cudaEventRecord(h->ev_chunk[c], h->cout));
         }
