@@ -27,8 +27,11 @@ struct tafv_comm {
   virtual void allreduce_sum_f64(int rank, double* d, int n, cudaStream_t st) = 0;
   virtual void allreduce_sum_i64(int rank, long long* d, int n, cudaStream_t st) = 0;
   // Halo exchange of `bytes_per_row` rows already packed in h.sendbuf (peer
-  // segments) into h.recvbuf (peer segments), ordered on `st`.
-  virtual void exchange(tafv_gpu& h, int bytes_per_row, cudaStream_t st) = 0;
+  // segments) into h.recvbuf (peer segments), ordered on `st`. scount /
+  // rcount (per peer, in h.peers order; null = whole segments): the leading
+  // rows of each segment that move (level-sorted lists).
+  virtual void exchange(tafv_gpu& h, int bytes_per_row, cudaStream_t st, const int* scount = nullptr,
+                        const int* rcount = nullptr) = 0;
   virtual void attach(int rank, tafv_gpu* h) {}
 };
 

@@ -37,6 +37,7 @@
 namespace tafv {
 
 constexpr int kMaxLevels = 16;
+constexpr int kMaxPeers = 4;  // level-sorted halo exchange lists (slab shards have <= 2 peers)
 
 // ---- device views --------------------------------------------------------
 struct MeshDev {
@@ -107,6 +108,12 @@ struct PlanDev {
   long long fi_count[kMaxLevels];
   long long fb_count[kMaxLevels];
   int sweep_changed[kMaxLevels];     // single-domain plan: Jacobi sweep i changed a level
+  // shards: the exchange lists of every peer sorted by level; prefix counts
+  // |{listed cells : tau <= l}| = the rows a phase at level l updates
+  int xs_prefix[kMaxPeers][kMaxLevels];
+  int xr_prefix[kMaxPeers][kMaxLevels];
+  long long xs_count[kMaxPeers][kMaxLevels];
+  long long xr_count[kMaxPeers][kMaxLevels];
 };
 
 // ---- staging: pure function of the committed/predicted state ---------------
@@ -1050,7 +1057,7 @@ struct CompactJob {
   int base;
 };
 struct CompactJobs {
-  CompactJob j[6];
+  CompactJob j[6 + 2 * kMaxPeers];
   int njobs;
 };
 
@@ -1230,6 +1237,15 @@ __global__ void k_store_plan(const PlanDev* __restrict__ src, PlanDev* dst) {
   const unsigned long long* a = reinterpret_cast<const unsigned long long*>(src);
   unsigned long long* b = reinterpret_cast<unsigned long long*>(dst);
   for (int i = threadIdx.x; i < (int)(sizeof(PlanDev) / 8); i += blockDim.x) b[i] = a[i];
+}
+
+// Shards: the levels of the listed cells (sort keys of the level-sorted
+// exchange lists), and the lists in level order from the compaction.
+__global__ void k_gather_keys(const int8_t* tau, const int* idx, int n, int8_t* key) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) key[i] = tau[idx[i]];
+}
+__global__ void k_permute_list(const int* idx, const int* pos, int n, int* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = idx[pos[i]];
 }
 
 __global__ void k_pack_rows(const double* src, const int* idx, int n, int width, double* dst) {

@@ -256,6 +256,16 @@ struct tafv_gpu {
   // boundary face of a deep cell), [F_int, F_own) the border ones; each
   // group has its own cadence-sorted K2 list (prefixes nfi / nfb_prefix)
   int F_int = 0;
+  // level-sorted exchange lists: each peer segment of the
+  // send / recv lists sorted by the cells' levels in every plan, so a phase
+  // at level l moves only the rows of cells with tau <= l (the rows it
+  // updated); xs / xr = the plan's per-peer prefix counts, host copies
+  bool xfilter = false;
+  int8_t *xkey_s = nullptr, *xkey_r = nullptr;
+  int *xpos_s = nullptr, *xpos_r = nullptr, *xsorted_s = nullptr, *xsorted_r = nullptr;
+  int* xcounts = nullptr;  // per-segment tile counts, [2 * peers][kMaxLevels * max tiles]
+  int xtile_stride = 0;
+  int xs[kMaxPeers][kMaxLevels] = {}, xr[kMaxPeers][kMaxLevels] = {};
   int* filist = nullptr;
   int* fblist = nullptr;
   int* fi_counts = nullptr;
@@ -335,6 +345,7 @@ struct tafv_gpu {
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf, d_cinv,
+                    xkey_s, xkey_r, xpos_s, xpos_r, xsorted_s, xsorted_r, xcounts,
                     klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, filist, fblist, fi_counts,
                     fb_counts};
     for (void* p : ptrs)
@@ -413,14 +424,16 @@ struct NcclComm final : tafv_comm {
   void allreduce_sum_i64(int, long long* d, int n, cudaStream_t st) override {
     NK(ncclAllReduce(d, d, n, ncclInt64, ncclSum, c, st));
   }
-  void exchange(tafv_gpu& h, int bpr, cudaStream_t st) override {
+  void exchange(tafv_gpu& h, int bpr, cudaStream_t st, const int* scount, const int* rcount) override {
     // grouped send/recv with every peer (the slab neighbours), one launch
     NK(ncclGroupStart());
-    for (const auto& p : h.peers) {
+    for (size_t q = 0; q < h.peers.size(); ++q) {
+      const auto& p = h.peers[q];
+      const int ns = scount ? scount[q] : p.nsend, nr = rcount ? rcount[q] : p.nrecv;
       char* sb = reinterpret_cast<char*>(h.sendbuf) + (size_t)p.soff * bpr;
       char* rb = reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr;
-      if (p.nsend) NK(ncclSend(sb, (size_t)p.nsend * bpr, ncclChar, p.rank, c, st));
-      if (p.nrecv) NK(ncclRecv(rb, (size_t)p.nrecv * bpr, ncclChar, p.rank, c, st));
+      if (ns) NK(ncclSend(sb, (size_t)ns * bpr, ncclChar, p.rank, c, st));
+      if (nr) NK(ncclRecv(rb, (size_t)nr * bpr, ncclChar, p.rank, c, st));
     }
     NK(ncclGroupEnd());
   }
@@ -477,19 +490,21 @@ struct LoopbackComm final : tafv_comm {
   void allreduce_sum_i64(int rank, long long* d, int n, cudaStream_t st) override {
     allreduce(i64, rank, d, n, st, [](long long a, long long b) { return a + b; });
   }
-  void exchange(tafv_gpu& h, int bpr, cudaStream_t st) override {
+  void exchange(tafv_gpu& h, int bpr, cudaStream_t st, const int* scount, const int* rcount) override {
     CK(cudaStreamSynchronize(st));  // my packed rows are in sendbuf
     barrier();
-    for (const auto& p : h.peers) {
+    for (size_t q = 0; q < h.peers.size(); ++q) {
+      const auto& p = h.peers[q];
       const tafv_gpu& g = *members[p.rank];
       const tafv_gpu::Peer* back = nullptr;
-      for (const auto& q : g.peers)
-        if (q.rank == h.rank) back = &q;
+      for (const auto& b : g.peers)
+        if (b.rank == h.rank) back = &b;
       if (!back || back->nsend != p.nrecv) throw Error{TAFV_ELOGIC, "loopback: mismatched exchange lists"};
-      if (p.nrecv)
+      const int nr = rcount ? rcount[q] : p.nrecv;
+      if (nr)
         CK(cudaMemcpyAsync(reinterpret_cast<char*>(h.recvbuf) + (size_t)p.roff * bpr,
                            reinterpret_cast<const char*>(g.sendbuf) + (size_t)back->soff * bpr,
-                           (size_t)p.nrecv * bpr, cudaMemcpyDeviceToDevice, st));
+                           (size_t)nr * bpr, cudaMemcpyDeviceToDevice, st));
     }
     CK(cudaStreamSynchronize(st));  // peers may reuse their send buffers
     barrier();
@@ -1072,6 +1087,19 @@ void alloc_state(tafv_gpu& h) {
   } else {
     h.klist = h.clist;
   }
+  if (h.sharded() && h.peers.size() <= (size_t)kMaxPeers && getenv("TAFV_FULL_HALO") == nullptr) {
+    h.xfilter = true;
+    h.xkey_s = dalloc<int8_t>(std::max(1, h.send_total));
+    h.xkey_r = dalloc<int8_t>(std::max(1, h.recv_total));
+    h.xpos_s = dalloc<int>(std::max(1, h.send_total));
+    h.xpos_r = dalloc<int>(std::max(1, h.recv_total));
+    h.xsorted_s = dalloc<int>(std::max(1, h.send_total));
+    h.xsorted_r = dalloc<int>(std::max(1, h.recv_total));
+    int maxseg = 1;
+    for (const auto& p : h.peers) maxseg = std::max(maxseg, std::max(p.nsend, p.nrecv));
+    h.xtile_stride = ((maxseg + kTile - 1) / kTile) * kMaxLevels;
+    h.xcounts = dalloc<int>((size_t)std::max<size_t>(1, 2 * h.peers.size()) * h.xtile_stride);
+  }
   h.nblk_last = h.sms * 16;
   h.partials = dalloc<DD>((size_t)h.nblk_last * 8);
   h.dplan = dalloc<PlanDev>(1);
@@ -1188,19 +1216,43 @@ void collect_times(tafv_gpu& h) {
 // join_now: the compute stream waits for the halo at once (trailing
 // corrector: the plan follows); otherwise the next K1 joins it before its
 // border cells (halo_join).
-void halo_rows(tafv_gpu& h, double* arr, int width, bool join_now) {
+// level >= 0 (level-sorted lists): only the rows of cells with tau <= level,
+// the ones the phase just updated, move.
+void halo_rows(tafv_gpu& h, double* arr, int width, bool join_now, int level = -1) {
   if (!h.sharded()) return;
-  if (h.send_total)
-    k_pack_rows<<<h.grid_for((long long)h.send_total * width, 256), 256, 0, h.st>>>(
-        arr, h.d_send_idx, h.send_total, width, h.sendbuf);
-  CK(cudaEventRecord(h.ev_pack, h.st));
-  CK(cudaStreamWaitEvent(h.cst, h.ev_pack, 0));
-  h.comm->exchange(h, width * (int)sizeof(double), h.cst);
-  if (h.recv_total)
-    k_unpack_rows<<<h.grid_for((long long)h.recv_total * width, 256), 256, 0, h.cst>>>(
-        h.recvbuf, h.d_recv_idx, h.recv_total, width, arr);
+  if (h.xfilter && level >= 0) {
+    int sc[kMaxPeers], rc[kMaxPeers];
+    for (size_t q = 0; q < h.peers.size(); ++q) {
+      const auto& pe = h.peers[q];
+      sc[q] = h.xs[q][level];
+      rc[q] = h.xr[q][level];
+      if (sc[q])
+        k_pack_rows<<<h.grid_for((long long)sc[q] * width, 256), 256, 0, h.st>>>(
+            arr, h.xsorted_s + pe.soff, sc[q], width, h.sendbuf + (size_t)pe.soff * width);
+    }
+    CK(cudaEventRecord(h.ev_pack, h.st));
+    CK(cudaStreamWaitEvent(h.cst, h.ev_pack, 0));
+    h.comm->exchange(h, width * (int)sizeof(double), h.cst, sc, rc);
+    for (size_t q = 0; q < h.peers.size(); ++q) {
+      const auto& pe = h.peers[q];
+      if (rc[q])
+        k_unpack_rows<<<h.grid_for((long long)rc[q] * width, 256), 256, 0, h.cst>>>(
+            h.recvbuf + (size_t)pe.roff * width, h.xsorted_r + pe.roff, rc[q], width, arr);
+    }
+    h.launches += 2 * (int64_t)h.peers.size();
+  } else {
+    if (h.send_total)
+      k_pack_rows<<<h.grid_for((long long)h.send_total * width, 256), 256, 0, h.st>>>(
+          arr, h.d_send_idx, h.send_total, width, h.sendbuf);
+    CK(cudaEventRecord(h.ev_pack, h.st));
+    CK(cudaStreamWaitEvent(h.cst, h.ev_pack, 0));
+    h.comm->exchange(h, width * (int)sizeof(double), h.cst);
+    if (h.recv_total)
+      k_unpack_rows<<<h.grid_for((long long)h.recv_total * width, 256), 256, 0, h.cst>>>(
+          h.recvbuf, h.d_recv_idx, h.recv_total, width, arr);
+    h.launches += 2;
+  }
   CK(cudaEventRecord(h.ev_halo, h.cst));
-  h.launches += 2;
   h.halo_pending = true;
   if (join_now) halo_join(h);
 }
@@ -1287,11 +1339,41 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
                            &h.dplan->fb_count[0], &h.dplan->nfb_prefix[0], h.F_int};
     jobs.njobs = 6;
   }
+  if (h.xfilter) {  // the exchange lists of every peer, sorted by level
+    if (h.send_total)
+      k_gather_keys<<<h.grid_for(h.send_total, 256), 256, 0, h.st>>>(h.tau, h.d_send_idx, h.send_total, h.xkey_s);
+    if (h.recv_total)
+      k_gather_keys<<<h.grid_for(h.recv_total, 256), 256, 0, h.st>>>(h.tau, h.d_recv_idx, h.recv_total, h.xkey_r);
+    h.launches += 2;
+    for (size_t q = 0; q < h.peers.size(); ++q) {
+      const auto& pe = h.peers[q];
+      for (int side = 0; side < 2; ++side) {
+        const int n = side ? pe.nrecv : pe.nsend, off = side ? pe.roff : pe.soff;
+        const int nt = std::max(1, (n + kTile - 1) / kTile);
+        int* cnt = h.xcounts + (2 * q + side) * (size_t)h.xtile_stride;
+        const int8_t* key = (side ? h.xkey_r : h.xkey_s) + off;
+        k_tile_count<<<nt, kCompactThreads, 0, h.st>>>(key, n, nkeys, cnt);
+        ++h.launches;
+        jobs.j[jobs.njobs++] = CompactJob{key, n, nt, cnt, (side ? h.xpos_r : h.xpos_s) + off,
+                                          side ? &h.dplan->xr_count[q][0] : &h.dplan->xs_count[q][0],
+                                          side ? &h.dplan->xr_prefix[q][0] : &h.dplan->xs_prefix[q][0], off};
+      }
+    }
+  }
   int tiles = 0;
   for (int q = 0; q < jobs.njobs; ++q) tiles += jobs.j[q].ntiles;
   k_tile_scan<<<jobs.njobs, 1024, 0, h.st>>>(jobs, nkeys, h.dplan, k1 ? 0 : 1);
   if (nkeys <= 5) k_tile_scatter_packed<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
   else k_tile_scatter<<<tiles, kCompactThreads, 0, h.st>>>(jobs, nkeys);
+  if (h.xfilter) {
+    if (h.send_total)
+      k_permute_list<<<h.grid_for(h.send_total, 256), 256, 0, h.st>>>(h.d_send_idx, h.xpos_s, h.send_total,
+                                                                        h.xsorted_s);
+    if (h.recv_total)
+      k_permute_list<<<h.grid_for(h.recv_total, 256), 256, 0, h.st>>>(h.d_recv_idx, h.xpos_r, h.recv_total,
+                                                                        h.xsorted_r);
+    h.launches += 2;
+  }
   h.launches += 3;
   if (h.sharded()) h.comm->allreduce_sum_i64(h.rank, &h.dplan->gcell_count[0], kMaxLevels, h.st);
   CK(cudaGetLastError());
@@ -1332,6 +1414,12 @@ void parse_plan(tafv_gpu& h) {
     h.gcount[l] = l < nkeys ? p.gcell_count[l] : 0;
     if (h.gcount[l] > 0) h.theta = l;  // theta = max level over all ranks
   }
+  if (h.xfilter)
+    for (size_t q = 0; q < h.peers.size(); ++q)
+      for (int l = 0; l < kMaxLevels; ++l) {
+        h.xs[q][l] = p.xs_prefix[q][l];
+        h.xr[q][l] = p.xr_prefix[q][l];
+      }
   h.has_plan = true;
 }
 
@@ -1650,7 +1738,7 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     h.launches += 3;
     // shards: the just-updated rows of owned cells to the peers' halos
     // (w_pred after a predictor, w after a corrector)
-    halo_rows(h, pred ? h.wp : h.w, P::NV, false);
+    halo_rows(h, pred ? h.wp : h.w, P::NV, false, level);
   }
 }
 
@@ -1689,7 +1777,9 @@ void enqueue_sweep_direct(tafv_gpu& h) {
 // captured once replays for every later iteration with the same theta.
 void run_sweep(tafv_gpu& h) {
   const Range r(h.sharded() ? "tafv.sweep.shard" : "tafv.sweep");
-  if (!h.use_graph || (h.sharded() && !h.comm->capturable())) {
+  // shards with level-sorted exchanges: the message sizes change with every
+  // plan, so the sweep is launched directly (NCCL counts are fixed in a graph)
+  if (!h.use_graph || (h.sharded() && (!h.comm->capturable() || h.xfilter))) {
     enqueue_sweep_direct(h);
     return;
   }
