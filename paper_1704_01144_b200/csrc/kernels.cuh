@@ -763,15 +763,20 @@ __global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD*
   __shared__ DD red[256];
   const int per = (nb + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
-#pragma unroll 1
-  for (int k = 0; k < NV; ++k) {
-    DD o{0.0, 0.0};
-    for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
-      double* p = bsum + (size_t)b * NV + k;
-      o = dd_add(o, *p);
-      *p = 0.0;
+  DD o[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) o[k] = DD{0.0, 0.0};
+  for (int b = b0 + threadIdx.x; b < b1; b += blockDim.x) {  // one pass over the rows
+    double* p = bsum + (size_t)b * NV;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      o[k] = dd_add(o[k], p[k]);
+      p[k] = 0.0;
     }
-    red[threadIdx.x] = o;
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    red[threadIdx.x] = o[k];
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
       if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
