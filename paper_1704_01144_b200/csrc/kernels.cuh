@@ -285,7 +285,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 #ifndef TAFV_K1_MINB
 #define TAFV_K1_MINB 5  // min resident 128-thread blocks/SM for K1 (register cap 102; measured best)
 #endif
-template <class P, int DEG>
+// TILE: the identity-phase instance (list == nullptr, Morton-brick staging);
+// a separate instantiation so each path is register-allocated on its own.
+template <class P, int DEG, bool TILE>
 __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, StateDev s,
                                                     const int* __restrict__ list,
                                                     const int* __restrict__ n_dev, int base, int front,
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
     for (int q = 0; q < GS; q += 4) st4(go + q, row[q], row[q + 1], row[q + 2], row[q + 3]);
   };
 #if TAFV_K1_TILE
-  if (DEG == 6 && list == nullptr) {
+  if constexpr (TILE && DEG == 6) {
     // Identity phase (every cell of [base, base + n) active): a block takes
     // 128 consecutive cells (a Morton brick), each thread stages its own cell
     // into shared memory once, and the neighbours inside the brick (~80 % of
@@ -468,17 +470,18 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       // measured slower: the barrier keeps the block's warps on one brick)
       __syncthreads();
     }
-    return;
-  }
+  } else
 #endif
-  for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
-    // rev: walk the items backwards, so this kernel starts on the rows its
-    // predecessor wrote last (still in L2); consecutive kernels alternate.
-    const int i = rev ? n - 1 - ii : ii;
-    const int c = list ? list[i] : base + i;
-    double we[NV];
-    stage_spec<NV>(s, c, front, pred, we);
-    cell(c, we, 0, 0, nullptr, nullptr, nullptr, 0);
+  {
+    for (int ii = blockIdx.x * blockDim.x + threadIdx.x; ii < n; ii += stride) {
+      // rev: walk the items backwards, so this kernel starts on the rows its
+      // predecessor wrote last (still in L2); consecutive kernels alternate.
+      const int i = rev ? n - 1 - ii : ii;
+      const int c = list ? list[i] : base + i;
+      double we[NV];
+      stage_spec<NV>(s, c, front, pred, we);
+      cell(c, we, 0, 0, nullptr, nullptr, nullptr, 0);
+    }
   }
 }
 
@@ -753,13 +756,31 @@ __global__ void __launch_bounds__(256) k_ledger(const int* __restrict__ bface, i
   }
 }
 
+// Fixed-order reduction of the per-block partials: block k reduces
+// component k (deterministic tree over a fixed number of partials) of the
+// state totals and, when the ledger runs, of its boundary outflows
+// (k_ledger_reduce's partials) into plan->bflux[k].
+__device__ __forceinline__ DD block_merge(const DD* part, int n, DD* red) {
+  DD a{0.0, 0.0};
+  for (int b = threadIdx.x; b < n; b += blockDim.x) a = dd_merge(a, part[b]);
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  const DD r = red[0];
+  __syncthreads();
+  return r;
+}
 // The ledger's per-face boundary outflows into per-block compensated
 // partials: block g reduces faces [g*per, (g+1)*per) (fixed shape, so the
 // sum is deterministic) component by component, clears them for the next
 // iteration and leaves lpart[k][g]. Spread over the whole device: one block
 // per component walking ~10^6 faces cost ~3 ms per iteration on config 4.
 template <int NV>
-__global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD* lpart) {
+__global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD* lpart, const DD* partials,
+                                                       int nblocks, PlanDev* plan, unsigned* ticket) {
   __shared__ DD red[256];
   const int per = (nb + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
@@ -785,25 +806,27 @@ __global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD*
     if (threadIdx.x == 0) lpart[(size_t)k * gridDim.x + blockIdx.x] = red[0];
     __syncthreads();
   }
+  // the last block to finish also does k_totals' work (one launch less on
+  // the trailing corrector's critical path)
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = 0; k < NV; ++k) {
+    const DD t = block_merge(partials + (size_t)k * nblocks, nblocks, red);
+    const DD o = block_merge(lpart + (size_t)k * gridDim.x, gridDim.x, red);
+    if (threadIdx.x == 0) {
+      plan->totals[k] = t.hi + t.lo;
+      plan->bflux[k] = o.hi + o.lo;
+    }
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
 }
 
-// Fixed-order reduction of the per-block partials: block k reduces
-// component k (deterministic tree over a fixed number of partials) of the
-// state totals and, when the ledger runs, of its boundary outflows
-// (k_ledger_reduce's partials) into plan->bflux[k].
-__device__ __forceinline__ DD block_merge(const DD* part, int n, DD* red) {
-  DD a{0.0, 0.0};
-  for (int b = threadIdx.x; b < n; b += blockDim.x) a = dd_merge(a, part[b]);
-  red[threadIdx.x] = a;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] = dd_merge(red[threadIdx.x], red[threadIdx.x + w]);
-    __syncthreads();
-  }
-  const DD r = red[0];
-  __syncthreads();
-  return r;
-}
 __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan, const DD* lpart,
                                                 int nl) {
   __shared__ DD red[256];

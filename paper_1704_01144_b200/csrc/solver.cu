@@ -162,6 +162,10 @@ struct tafv_gpu {
   double4* fdx = nullptr;  // see MeshDev::fdx
   bool slot_geo = true;
   bool slot_n = true, slot_dx = true;  // A/B: per-slot normals / limiter offsets individually
+  // identity-phase K1 in Morton bricks (k_grad_limit<.., true>): -1 auto
+  // (meshes of >= 4M cells, where it measured -2 % K1; +3-4 % on 0.26M / 1M)
+  int k1_tile = -1;
+  bool use_k1_tile() const { return deg6 && (k1_tile > 0 || (k1_tile < 0 && n_own >= (4 << 20))); }
   bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
   // run_batch lanes: a twin handle sharing this one's (read-only) mesh arrays
@@ -194,6 +198,7 @@ struct tafv_gpu {
   uint8_t* fflag = nullptr;
   double *dtmax = nullptr, *blockmin = nullptr;
   unsigned* dt_ticket = nullptr;  // last-block ticket of k_dt_max
+  unsigned* led_ticket = nullptr; // last-block ticket of k_ledger_reduce
   int nblk_dt = 0;
   int *cell_counts = nullptr, *face_counts = nullptr;
   int ntile_c = 0, ntile_f = 0;
@@ -343,7 +348,7 @@ struct tafv_gpu {
     }
     void* ptrs[] = {w,     W,        wp,       bsum,  lpart,
                     grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
-                    fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
+                    fflag, dt_ticket, led_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf, d_cinv,
                     xkey_s, xkey_r, xpos_s, xpos_r, xsorted_s, xsorted_r, xcounts,
                     klist != clist ? klist : nullptr, k1_counts, kblist, kb_counts, filist, fblist, fi_counts,
@@ -1055,6 +1060,8 @@ void alloc_state(tafv_gpu& h) {
   h.fflag = dalloc<uint8_t>(((size_t)N + 3) & ~(size_t)3);  // word-addressed by k_face_cadence
   CK(cudaMemset(h.fflag, 0, ((size_t)N + 3) & ~(size_t)3));
   h.dt_ticket = dalloc<unsigned>(1);
+  h.led_ticket = dalloc<unsigned>(1);
+  CK(cudaMemset(h.led_ticket, 0, sizeof(unsigned)));
   CK(cudaMemset(h.dt_ticket, 0, sizeof(unsigned)));
   h.cad = dalloc<int8_t>(F);
   CK(cudaMemset(h.tau, 0, N));
@@ -1116,7 +1123,7 @@ void alloc_state(tafv_gpu& h) {
 template <class P, int DEG>
 void set_grids_t(tafv_gpu& h) {
   int b1 = 0, b2 = 0, b3 = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_grad_limit<P, DEG>, 128, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_grad_limit<P, DEG, false>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_face_flux<P, true>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_gather_update<P, true, false, DEG>, 128, 0));
   h.grid_k1 = h.sms * std::max(1, b1);
@@ -1669,7 +1676,11 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
   timed(h, tafv_gpu::kK1, [&] {
-    k_grad_limit<P, DEG><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
+    // identity phases (kl == nullptr) of hex meshes: the Morton-brick instance
+    if (DEG == 6 && kl == nullptr && h.use_k1_tile())
+      k_grad_limit<P, DEG, true><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
+    else
+      k_grad_limit<P, DEG, false><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
   }, na, nf, nfr);
   const PlanDev* cpl = h.dplan;
   // shards with a halo: deep / border K1 lists and interior / border K2
@@ -1690,7 +1701,10 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
     halo_join(h);
     const int gb = fixed ? h.grid_k1 : h.grid_for(h.n_k1 - h.n_deep, 128);
     timed(h, tafv_gpu::kK1, [&] {
-      k_grad_limit<P, DEG><<<gb, 128, 0, h.st>>>(md, sd, kbl, nkbp, h.n_deep, front, pred ? 1 : 0, 0);
+      if (DEG == 6 && kbl == nullptr && h.use_k1_tile())
+        k_grad_limit<P, DEG, true><<<gb, 128, 0, h.st>>>(md, sd, kbl, nkbp, h.n_deep, front, pred ? 1 : 0, 0);
+      else
+        k_grad_limit<P, DEG, false><<<gb, 128, 0, h.st>>>(md, sd, kbl, nkbp, h.n_deep, front, pred ? 1 : 0, 0);
     }, 0, 0, 0);
     ++h.launches;
   }
@@ -1715,12 +1729,12 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
                                                                           h.dplan, h.partials, 0);
     }, na, nf, 0);
     ledger_join(h);
-    if (h.NB) {
-      k_ledger_reduce<P::NV><<<h.nblk_led, 256, 0, h.st>>>(h.bsum, h.NB, h.lpart);
-      ++h.launches;
-    }
-    k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, h.NB ? h.lpart : nullptr, h.nblk_led);
-    h.launches += 4;
+    if (h.NB)  // the ledger's outflow partials; its last block also writes the totals
+      k_ledger_reduce<P::NV><<<h.nblk_led, 256, 0, h.st>>>(h.bsum, h.NB, h.lpart, h.partials, h.nblk_last,
+                                                            h.dplan, h.led_ticket);
+    else  // no transmissive face: the totals alone
+      k_totals<<<P::NV, 256, 0, h.st>>>(h.partials, h.nblk_last, h.dplan, nullptr, 1);
+    h.launches += 4;  // K1, K2, K3 and the totals
     if (h.sharded()) {
       h.comm->allreduce_sum_f64(h.rank, h.dplan->totals, P::NV, h.st);
       h.comm->allreduce_sum_f64(h.rank, h.dplan->bflux, P::NV, h.st);
@@ -2345,7 +2359,7 @@ static void repartition(tafv_gpu* h, const tafv_mesh_view* gm, const int32_t* ro
   const bool use_graph = h->use_graph, plan_graph_on = h->plan_graph_on, slot_geo = h->slot_geo,
              slot_n = h->slot_n, slot_dx = h->slot_dx, face_dx = h->face_dx, alt_dir = h->alt_dir,
              iwin_alias = h->iwin_alias;
-  const int dl_stream = h->dl_stream, batch_lanes = h->batch_lanes;
+  const int dl_stream = h->dl_stream, batch_lanes = h->batch_lanes, k1_tile = h->k1_tile;
   const tafv_mesh_view* rep_mesh = h->rep_mesh;
   const int rep_every = h->rep_every, rep_axis = h->rep_axis;
   h->release();
@@ -2360,6 +2374,7 @@ static void repartition(tafv_gpu* h, const tafv_mesh_view* gm, const int32_t* ro
   h->iwin_alias = iwin_alias;
   h->dl_stream = dl_stream;
   h->batch_lanes = batch_lanes;
+  h->k1_tile = k1_tile;
   h->rep_mesh = rep_mesh;
   h->rep_every = rep_every;
   h->rep_axis = rep_axis;
@@ -2514,6 +2529,7 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->d_fperm = h.d_fperm;
     t->slot_geo = h.slot_geo;
     t->slot_n = h.slot_n;
+    t->k1_tile = h.k1_tile;
     t->slot_dx = h.slot_dx;
     t->face_dx = h.face_dx;
     t->iwin_alias = h.iwin_alias;
@@ -2935,6 +2951,9 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+      drop_graphs(*h);
+    } else if (n == "k1_tile") {
+      h->k1_tile = (int)value;
       drop_graphs(*h);
     } else if (n == "slot_n") {
       h->slot_n = value != 0;

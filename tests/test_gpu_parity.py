@@ -713,6 +713,47 @@ def test_sharded_repartition_by_level_cost_bitwise(gpu):
     assert out[0][3] == n1 + n2
 
 
+@pytest.mark.parametrize("cid,scale,iters", [(2, 5, 4), (4, 20, 3), (3, 10, 3)])
+def test_k1_brick_path_bitwise(cid, scale, iters, gpu):
+    """The identity-phase K1 in Morton bricks (k_grad_limit<.., true>,
+    neighbours inside the brick read from shared memory; chosen by default
+    only on meshes of >= 4M cells) is bitwise the per-cell path, on a single
+    domain and on loopback shards (deep / border identity lists)."""
+    cfg = configs.get(cid, scale)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    out = {}
+    for tile in (0, 1):
+        g = Solver(mesh, "euler")
+        g.set_flag("k1_tile", tile)
+        g.set_state(w0)
+        recs = g.reference_integrate(cfg.options(), iters)
+        out[tile] = (g.get_state(), [r["level_cells"] for r in recs])
+        g.close()
+    np.testing.assert_array_equal(out[0][0][0], out[1][0][0])
+    np.testing.assert_array_equal(out[0][0][1], out[1][0][1])
+    assert out[0][1] == out[1][1]
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    roc = shard.partition_slabs(mesh, 2, axis=0)
+    comm = Comm.loopback(2)
+    solvers = [Solver(mesh, "euler", shard=(roc, r, comm)) for r in range(2)]
+    res = {}
+
+    def body(r):
+        solvers[r].set_flag("k1_tile", 1)
+        solvers[r].set_state(w0)
+        solvers[r].reference_integrate(cfg.options(), iters)
+        res[r] = solvers[r].get_state()[0]
+
+    _threads(2, body)
+    for sv in solvers:
+        sv.close()
+    comm.close()
+    w = sum(res[r] * (roc == r)[:, None] for r in range(2))
+    np.testing.assert_array_equal(w, out[0][0][0])
+
+
 def _threads(world, body):
     errs = []
 
