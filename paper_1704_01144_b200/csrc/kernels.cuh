@@ -779,8 +779,7 @@ __device__ __forceinline__ DD block_merge(const DD* part, int n, DD* red) {
 // iteration and leaves lpart[k][g]. Spread over the whole device: one block
 // per component walking ~10^6 faces cost ~3 ms per iteration on config 4.
 template <int NV>
-__global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD* lpart, const DD* partials,
-                                                       int nblocks, PlanDev* plan, unsigned* ticket) {
+__global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD* lpart) {
   __shared__ DD red[256];
   const int per = (nb + gridDim.x - 1) / gridDim.x;
   const int b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
@@ -806,25 +805,6 @@ __global__ void __launch_bounds__(256) k_ledger_reduce(double* bsum, int nb, DD*
     if (threadIdx.x == 0) lpart[(size_t)k * gridDim.x + blockIdx.x] = red[0];
     __syncthreads();
   }
-  // the last block to finish also does k_totals' work (one launch less on
-  // the trailing corrector's critical path)
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int k = 0; k < NV; ++k) {
-    const DD t = block_merge(partials + (size_t)k * nblocks, nblocks, red);
-    const DD o = block_merge(lpart + (size_t)k * gridDim.x, gridDim.x, red);
-    if (threadIdx.x == 0) {
-      plan->totals[k] = t.hi + t.lo;
-      plan->bflux[k] = o.hi + o.lo;
-    }
-  }
-  if (threadIdx.x == 0) *ticket = 0u;
 }
 
 __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks, PlanDev* plan, const DD* lpart,
