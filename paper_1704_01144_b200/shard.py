@@ -133,3 +133,81 @@ def initial_level_cost(mesh, w, opt):
     """Per-cell level cost 2^(theta - tau) of the initial plan: the weights
     of the slab cut (DistDriver::repartition, exchange.cpp:598-603)."""
     return level_cost_weights(initial_levels(mesh, w, opt))
+
+
+# ---- per-rank slab windows (no rank builds the global mesh) -----------------
+
+def _dt_max_host(mesh, w, opt, gamma=1.4):
+    """dt_max = cfl h / (|u| + c) on the host (slab-cut weights only)."""
+    w = np.asarray(w, dtype=np.float64).reshape(len(mesh["vol"]), -1)
+    rho = w[:, 0]
+    u = w[:, 1:4] / rho[:, None]
+    p = (gamma - 1.0) * (w[:, 4] - 0.5 * rho * (u * u).sum(axis=1))
+    speed = np.sqrt((u * u).sum(axis=1)) + np.sqrt(gamma * np.maximum(p, 0.0) / rho)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.where(speed > 0, np.minimum(opt.dt_cap, opt.cfl * mesh["chl"] / speed), opt.dt_cap)
+
+
+def plane_costs(cfg, opt, i0, i1, allreduce_min, allreduce_max, allreduce_sum):
+    """Level cost 2^(theta - raw) of the initial state summed per x plane of
+    a tensor-product config, each rank generating only the planes [i0, i1)
+    (a provisional slab) and the collectives combining them (the raw levels,
+    unsmoothed: smoothing only raises the cost near level jumps; the cut
+    needs balance, not bits). Returns the per-plane costs of the whole
+    lattice on every rank."""
+    nx, ny, nz = cfg.n
+    m = cfg.mesh(window=(i0, i1, 0, ny, 0, nz))
+    dtm = _dt_max_host(m, cfg.initial_state(m), opt)
+    dmin = allreduce_min(float(dtm.min()) if len(dtm) else float("inf"))
+    ratio = dtm / dmin
+    raw = np.clip(np.where(ratio >= 1.0, np.frexp(ratio)[1] - 1, 0), 0, opt.theta_max).astype(np.int64)
+    theta = int(allreduce_max(float(raw.max()) if len(raw) else 0.0))
+    cost = np.ldexp(1.0, theta - raw)
+    plane = np.arange(len(cost)) % max(1, i1 - i0) + i0
+    mine = np.bincount(plane, weights=cost, minlength=nx)
+    return allreduce_sum(mine)
+
+
+def slab_cuts(costs, nranks):
+    """Contiguous plane ranges of balanced cost: cuts[r] .. cuts[r + 1]."""
+    cum = np.concatenate([[0.0], np.cumsum(costs)])
+    cuts = [0]
+    for r in range(1, nranks):
+        cuts.append(int(np.clip(np.searchsorted(cum, cum[-1] * r / nranks), cuts[-1] + 1, len(costs) - (nranks - r))))
+    cuts.append(len(costs))
+    return np.asarray(cuts, dtype=np.int64)
+
+
+def slab_window(cfg, cuts, rank, rings=2):
+    """Rank `rank`'s x slab [cuts[rank], cuts[rank + 1]) of a tensor-product
+    (unpermuted) config plus `rings` planes on each side, generated as a
+    window of the lattice (tafv_mesh_hex_window: the cells and faces are
+    bitwise the full mesh's, in the same relative order, so the shard built
+    from it is bitwise the shard of the global mesh). Returns (window mesh,
+    rank_of_cell over the window's cells, global ids of the window's cells)."""
+    if cfg.permute:
+        raise ValueError("slab_window: permuted configs have no lattice windows")
+    nx, ny, nz = cfg.n
+    i0, i1 = max(0, int(cuts[rank]) - rings), min(nx, int(cuts[rank + 1]) + rings)
+    mesh = cfg.mesh(window=(i0, i1, 0, ny, 0, nz))
+    wx = i1 - i0
+    ids = np.arange(wx * ny * nz, dtype=np.int64)
+    plane = ids % wx + i0
+    roc = (np.searchsorted(np.asarray(cuts), plane, side="right") - 1).astype(np.int32)
+    gid = (ids // wx) * nx + plane
+    return mesh, roc, gid
+
+
+def distributed_slab_window(cfg, opt, rank, nranks, allreduce):
+    """The rank's slab window of a multi-process run: provisional uniform
+    slabs, per-plane level costs combined with `allreduce(value, op)` (op in
+    "min", "max", "sum"; value a float or a numpy array), balanced cuts,
+    then the rank's own window. Returns (mesh, rank_of_cell, global ids,
+    cuts); every rank gets the same cuts."""
+    nx = cfg.n[0]
+    b = [round(r * nx / nranks) for r in range(nranks + 1)]
+    costs = plane_costs(cfg, opt, b[rank], b[rank + 1], lambda v: allreduce(v, "min"),
+                        lambda v: allreduce(v, "max"), lambda v: allreduce(v, "sum"))
+    cuts = slab_cuts(costs, nranks)
+    mesh, roc, gid = slab_window(cfg, cuts, rank)
+    return mesh, roc, gid, cuts

@@ -754,6 +754,62 @@ def test_k1_brick_path_bitwise(cid, scale, iters, gpu):
     np.testing.assert_array_equal(w, out[0][0][0])
 
 
+@pytest.mark.parametrize("cid,scale,world,iters", [(3, 10, 3, 3), (4, 20, 2, 2)])
+def test_window_slab_shards_bitwise(cid, scale, world, iters, gpu):
+    """Per-rank slab windows (shard.slab_window: each rank generates only its
+    slab + 2 planes of the lattice, no rank builds the global mesh; cuts by
+    the initial level cost per plane, shard.plane_costs over loopback
+    collectives) reproduce the single-domain run on the global mesh bitwise."""
+    from paper_1704_01144_b200 import shard
+    from paper_1704_01144_b200.api import Comm
+    cfg = configs.get(cid, scale)
+    opt = cfg.options()
+    nx = cfg.n[0]
+    bounds = [round(r * nx / world) for r in range(world + 1)]
+    # the collectives of plane_costs over the ranks (torch.distributed in the
+    # bench): a first pass collects the local minima / maxima, a second one
+    # uses the global values and sums the per-plane costs
+    dmins, thetas = [], []
+    for r in range(world):
+        shard.plane_costs(cfg, opt, bounds[r], bounds[r + 1], lambda v: dmins.append(v) or v,
+                          lambda v: thetas.append(v) or v, lambda v: v)
+    dmin, theta = min(dmins), max(thetas)
+    costs = sum(shard.plane_costs(cfg, opt, bounds[r], bounds[r + 1], lambda v: dmin, lambda v: theta,
+                                  lambda v: v) for r in range(world))
+    cuts = shard.slab_cuts(costs, world)
+    comm = Comm.loopback(world)
+    wins = [shard.slab_window(cfg, cuts, r) for r in range(world)]
+    solvers = [Solver(wins[r][0], "euler", shard=(wins[r][1], r, comm)) for r in range(world)]
+    res = {}
+
+    def body(r):
+        m, roc, gid = wins[r]
+        solvers[r].set_state(cfg.initial_state(m))
+        recs = solvers[r].reference_integrate(opt, iters)
+        w, W = solvers[r].get_state()[:2]
+        own = roc == r
+        res[r] = (gid[own], w[own], W[own], recs)
+
+    _threads(world, body)
+    for sv in solvers:
+        sv.close()
+    comm.close()
+    mesh = cfg.mesh()
+    g = Solver(mesh, "euler")
+    g.set_state(cfg.initial_state(mesh))
+    ref = g.reference_integrate(opt, iters)
+    wr, Wr = g.get_state()[:2]
+    seen = np.zeros(len(mesh["vol"]), dtype=int)
+    for r in range(world):
+        gid, w, W, recs = res[r]
+        np.testing.assert_array_equal(w, wr[gid])
+        np.testing.assert_array_equal(W, Wr[gid])
+        seen[gid] += 1
+        assert [x["dt"] for x in recs] == [x["dt"] for x in ref]
+        assert [x["level_cells"] for x in recs] == [x["level_cells"] for x in ref]
+    assert (seen == 1).all()
+
+
 def _threads(world, body):
     errs = []
 
