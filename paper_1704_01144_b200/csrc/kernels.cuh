@@ -485,6 +485,230 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
   }
 }
 
+// ---- K1 for identity phases of hex meshes: brick streams by bulk copies ------
+// A block takes a Morton brick of 128 consecutive cells and ONE elected thread
+// starts bulk copies (cp.async.bulk, the TMA engine; one mbarrier collects the
+// bytes) of every contiguous stream the brick reads: the cells' staged rows
+// (in an identity phase every window boundary lies on the front, so the
+// staged row IS w in a predictor / w_pred in a corrector, kernels.cpp:31-44),
+// centroids, 1/V, the CSR slots (neighbour, face) and a window of the face
+// arrays {normal, area} and centroids starting at the first face whose left
+// cell is in the brick (faces are grouped by left cell, so the window holds
+// the brick's +side faces and, through the neighbours inside the brick, ~80 %
+// of its -side ones). The per-cell arithmetic is k_grad_limit's (per-face
+// geometry: scale = sign * area, offset = face centroid - cell centroid, the
+// values the per-slot streams store); every operand that is in the brick is
+// read from shared memory, the rest (neighbour rows / faces outside the
+// window) through a generic pointer that selects global memory, so a warp
+// does not diverge on it. No global load sits on a cell's dependent chain
+// except those out-of-brick rows, and the per-slot geometry streams (384 of
+// the 580 DRAM bytes k_grad_limit reads per cell) are not read at all. Other
+// resident blocks compute while a block waits for its copies (one stage per
+// block: double buffering would halve the resident warps for the same
+// shared memory).
+#ifndef TAFV_K1B_MINB
+#define TAFV_K1B_MINB 5
+#endif
+constexpr int kBrick = 128;      // cells per brick = threads per block
+constexpr int kBrickFaces = 448; // face window (3 +side faces per cell and boundary slack), even
+template <int NV>
+struct BrickSmem {  // byte offsets into the dynamic shared memory (16-byte aligned parts)
+  static constexpr int row = 0;
+  static constexpr int cen = row + kBrick * NV * 8;
+  static constexpr int ivol = cen + kBrick * 24;
+  static constexpr int nb = ivol + kBrick * 8;
+  static constexpr int af = nb + kBrick * 24;
+  static constexpr int geo = (af + kBrick * 24 + 31) & ~31;
+  static constexpr int fcen = geo + kBrickFaces * 32;
+  static constexpr int bytes = fcen + kBrickFaces * 24;
+};
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before the async writes
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+// brick_f0[b] = first face whose left cell is >= 128 b (k_brick_f0); cells
+// [0, *n_dev) active, all with 6 slots.
+template <class P>
+__global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(MeshDev m, StateDev s,
+                                                                           const int* __restrict__ brick_f0,
+                                                                           const int* __restrict__ n_dev,
+                                                                           int pred, int rev) {
+  constexpr int NV = P::NV, D = P::DIM, B = kBrick;
+  using L = BrickSmem<NV>;
+  extern __shared__ __align__(128) unsigned char brick_smem[];
+  double* s_row = reinterpret_cast<double*>(brick_smem + L::row);
+  double* s_cen = reinterpret_cast<double*>(brick_smem + L::cen);
+  double* s_ivol = reinterpret_cast<double*>(brick_smem + L::ivol);
+  int* s_nb = reinterpret_cast<int*>(brick_smem + L::nb);
+  int* s_af = reinterpret_cast<int*>(brick_smem + L::af);
+  double* s_geo = reinterpret_cast<double*>(brick_smem + L::geo);
+  double* s_fcen = reinterpret_cast<double*>(brick_smem + L::fcen);
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  unsigned parity = 0;
+  const int n = *n_dev;
+  const int nbricks = (n + B - 1) / B;
+  const double* __restrict__ src = pred ? s.w : s.wp;
+  for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
+    // rev: walk the bricks backwards (the rows the predecessor wrote last are still in L2)
+    const int bb = rev ? nbricks - 1 - b : b;
+    const int lo = bb * B;
+    const int cnt = min(B, n - lo);
+    // face window [fs, fs + fcnt): even start and count (24-byte centroid rows, 16-byte copies)
+    const int f0 = brick_f0[bb], f1 = brick_f0[bb + 1];
+    const int fs = f0 & ~1;
+    int fcnt = min(f1, fs + kBrickFaces) - fs;
+    if (fcnt & 1) fcnt += fs + fcnt < m.n_faces ? 1 : -1;
+    if (fcnt < 0) fcnt = 0;
+    if (cnt == B) {
+      if (tid == 0) {
+        mbar_expect(&bar, (unsigned)(B * NV * 8 + B * 24 + B * 8 + B * 24 + B * 24 + fcnt * 56));
+        bulk_copy(s_row, src + (size_t)lo * NV, B * NV * 8, &bar);
+        bulk_copy(s_nb, m.adj_nb + 6 * (size_t)lo, B * 24, &bar);
+        bulk_copy(s_af, m.adj_face + 6 * (size_t)lo, B * 24, &bar);
+        if (fcnt) {
+          bulk_copy(s_geo, m.geo + fs, (unsigned)fcnt * 32, &bar);
+          bulk_copy(s_fcen, m.fcen + 3 * (size_t)fs, (unsigned)fcnt * 24, &bar);
+        }
+        bulk_copy(s_cen, m.cen + 3 * (size_t)lo, B * 24, &bar);
+        bulk_copy(s_ivol, m.ivol + lo, B * 8, &bar);
+      }
+      mbar_wait(&bar, parity);
+      parity ^= 1u;
+    } else {  // the tail brick: plain cooperative copies
+      for (int i = tid; i < cnt * NV; i += B) s_row[i] = src[(size_t)lo * NV + i];
+      for (int i = tid; i < cnt * 6; i += B) {
+        s_nb[i] = m.adj_nb[6 * (size_t)lo + i];
+        s_af[i] = m.adj_face[6 * (size_t)lo + i];
+      }
+      for (int i = tid; i < cnt * 3; i += B) s_cen[i] = m.cen[3 * (size_t)lo + i];
+      for (int i = tid; i < cnt; i += B) s_ivol[i] = m.ivol[lo + i];
+      for (int i = tid; i < fcnt * 4; i += B) s_geo[i] = reinterpret_cast<const double*>(m.geo + fs)[i];
+      for (int i = tid; i < fcnt * 3; i += B) s_fcen[i] = m.fcen[3 * (size_t)fs + i];
+      __syncthreads();
+    }
+    if (tid < cnt) {
+      const int c = lo + tid;
+      double we[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) we[k] = s_row[tid * NV + k];
+      double g[NV][D];
+      double wmin[NV], wmax[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) g[k][d] = 0.0;
+        wmin[k] = __longlong_as_double(0x7ff0000000000000ll);
+        wmax[k] = __longlong_as_double((long long)0xfff0000000000000ull);
+      }
+      bool any = false;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const int nb = s_nb[tid * 6 + t];
+        const int ef = s_af[tid * 6 + t];
+        const int f = slot_face(ef);
+        const unsigned fi = (unsigned)(f - fs);
+        const double* gp = fi < (unsigned)fcnt ? s_geo + 4 * fi : reinterpret_cast<const double*>(m.geo + f);
+        const double2 g01 = *reinterpret_cast<const double2*>(gp);
+        const double2 g23 = *reinterpret_cast<const double2*>(gp + 2);
+        const double scale = slot_sign(ef) * g23.y;
+        double wf[NV];
+        if (nb >= 0) {
+          const unsigned ni = (unsigned)(nb - lo);
+          const double* rp = ni < (unsigned)cnt ? s_row + ni * NV : src + (size_t)nb * NV;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            const double wn = rp[k];
+            wf[k] = 0.5 * (we[k] + wn);
+            wmin[k] = smin(wmin[k], wn);
+            wmax[k] = smax(wmax[k], wn);
+          }
+          any = true;
+        } else {
+#pragma unroll
+          for (int k = 0; k < NV; ++k) wf[k] = we[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          g[k][0] += wf[k] * g01.x * scale;
+          g[k][1] += wf[k] * g01.y * scale;
+          if (D == 3) g[k][D - 1] += wf[k] * g23.x * scale;
+        }
+      }
+      const double inv_v = s_ivol[tid];
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int d = 0; d < D; ++d) g[k][d] = g[k][d] * inv_v;
+      if (any) {
+        const double cc0 = s_cen[3 * tid], cc1 = s_cen[3 * tid + 1], cc2 = s_cen[3 * tid + 2];
+        double alpha[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          alpha[k] = 1.0;
+          wmax[k] = wmax[k] - we[k];     // hp: headroom above
+          wmin[k] = -(wmin[k] - we[k]);  // hn: headroom below, negated (exact)
+        }
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          const int f = slot_face(s_af[tid * 6 + t]);
+          const unsigned fi = (unsigned)(f - fs);
+          const double* fc = fi < (unsigned)fcnt ? s_fcen + 3 * fi : m.fcen + 3 * (size_t)f;
+          const double dx0 = fc[0] - cc0, dx1 = fc[1] - cc1, dx2 = fc[2] - cc2;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) {
+            double delta = g[k][0] * dx0 + g[k][1] * dx1;
+            if (D == 3) delta = delta + g[k][D - 1] * dx2;
+            alpha[k] = bj_update(alpha[k], delta, wmax[k], wmin[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+#pragma unroll
+          for (int d = 0; d < D; ++d) g[k][d] *= alpha[k];
+      }
+      constexpr int GS = GradRow<NV>::S;
+      double row[GS];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        row[3 * k] = g[k][0];
+        row[3 * k + 1] = g[k][1];
+        row[3 * k + 2] = D == 3 ? g[k][D - 1] : 0.0;
+      }
+#pragma unroll
+      for (int q = 3 * NV; q < GS; ++q) row[q] = 0.0;
+      double* go = s.grad + (size_t)c * GS;
+#pragma unroll
+      for (int q = 0; q < GS; q += 4) st4(go + q, row[q], row[q + 1], row[q + 2], row[q + 3]);
+    }
+    __syncthreads();  // every read of the stage before the next brick's copies
+  }
+}
+
+// First face whose left cell is >= 128 b, b in [0, nb] (faces grouped by left
+// cell: a binary search; on any other order the window is merely a worse cache).
+__global__ void k_brick_f0(const int2* __restrict__ lr, int F, int nb, int* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  const long long key = (long long)b * kBrick;
+  int lo = 0, hi = F;
+  while (lo < hi) {
+    const int mid = lo + (hi - lo) / 2;
+    if (lr[mid].x < key) lo = mid + 1;
+    else hi = mid;
+  }
+  out[b] = lo;
+}
+
 // kernels.cpp:25-27 with the z term appended left to right; d = to - from.
 template <int D>
 __device__ __forceinline__ double extrapolate_d(double w, const double* g, const double* d) {

@@ -71,6 +71,9 @@ void check_cuda(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw Error{TAFV_ECUDA, std::string(where) + ": " + cudaGetErrorString(e)};
 }
 #define CK(x) check_cuda((x), #x)
+#ifndef TAFV_K1_BRICK_AUTO
+#define TAFV_K1_BRICK_AUTO (1 << 30)  // auto threshold (owned cells) of the brick K1; off until measured
+#endif
 
 void require(bool cond, const char* what) {
   if (!cond) throw Error{TAFV_EINVAL, what};
@@ -166,6 +169,14 @@ struct tafv_gpu {
   // (meshes of >= 4M cells, where it measured -2 % K1; +3-4 % on 0.26M / 1M)
   int k1_tile = -1;
   bool use_k1_tile() const { return deg6 && (k1_tile > 0 || (k1_tile < 0 && n_own >= (4 << 20))); }
+  // identity-phase K1 with the brick's streams bulk-copied into shared memory
+  // (k_grad_limit_brick; per-face geometry windows): -1 auto, 0 off, 1 on
+  int k1_brick = -1;
+  int* brick_f0 = nullptr;  // [ceil(n_k1 / 128) + 1] first face by left cell (mesh, shared with the twin)
+  int grid_k1b = 0;
+  bool use_k1_brick() const {
+    return deg6 && brick_f0 && (k1_brick > 0 || (k1_brick < 0 && n_own >= (TAFV_K1_BRICK_AUTO)));
+  }
   bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
   // run_batch lanes: a twin handle sharing this one's (read-only) mesh arrays
@@ -341,7 +352,7 @@ struct tafv_gpu {
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     if (owns_mesh) {
       void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
-                           d_cperm, d_fperm, bface};
+                           d_cperm, d_fperm, bface, brick_f0};
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
@@ -1026,6 +1037,13 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
                  const uint8_t* touch = nullptr) {
   if (getenv("TAFV_HOST_UPLOAD") != nullptr) upload_mesh_host(h, mv, cls, touch);
   else upload_mesh_device(h, mv, cls, touch);
+  if (h.deg6) {  // face windows of the brick K1 (k_grad_limit_brick)
+    const int nb = (h.n_k1 + kBrick - 1) / kBrick;
+    h.brick_f0 = dalloc<int>((size_t)nb + 1);
+    k_brick_f0<<<(nb + 256) / 256, 256, 0, h.st>>>(h.lr, h.F, nb, h.brick_f0);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h.st));
+  }
 }
 
 void alloc_state(tafv_gpu& h) {
@@ -1124,6 +1142,16 @@ void set_grids_t(tafv_gpu& h) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_face_flux<P, true>, 128, 0));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k_gather_update<P, true, false, DEG>, 128, 0));
   h.grid_k1 = h.sms * std::max(1, b1);
+  if (DEG == 6) {
+    // brick K1: dynamic shared memory (one stage per block), carve-out at its maximum
+    constexpr int smem = BrickSmem<P::NV>::bytes;
+    CK(cudaFuncSetAttribute(k_grad_limit_brick<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(k_grad_limit_brick<P>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                            cudaSharedmemCarveoutMaxShared));
+    int bb = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k_grad_limit_brick<P>, kBrick, smem));
+    h.grid_k1b = h.sms * std::max(1, bb);
+  }
   // trailing corrector: exactly one wave of resident blocks (its partials
   // buffer holds sms * 16 blocks)
   int bl = 0;
@@ -1673,8 +1701,13 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   const int g3 = fixed ? h.grid_k3 : h.grid_for((na + CPB - 1) / CPB * 128, 128);
   const long long nfr = level < h.theta ? h.frcount[level] : 0;
   timed(h, tafv_gpu::kK1, [&] {
-    // identity phases (kl == nullptr) of hex meshes: the Morton-brick instance
-    if (DEG == 6 && kl == nullptr && h.use_k1_tile())
+    // identity phases (kl == nullptr) of hex meshes: the bulk-copy brick kernel
+    // (single list: cells [0, n) lead the internal order), else the Morton-brick instance
+    if (DEG == 6 && kl == nullptr && !(h.sharded() && h.klist != h.clist) && h.use_k1_brick())
+      k_grad_limit_brick<P><<<fixed ? h.grid_k1b : std::min<long long>(h.grid_k1b, (nk + kBrick - 1) / kBrick),
+                              kBrick, BrickSmem<P::NV>::bytes, h.st>>>(md, sd, h.brick_f0, nkp, pred ? 1 : 0,
+                                                                      h.next_dir());
+    else if (DEG == 6 && kl == nullptr && h.use_k1_tile())
       k_grad_limit<P, DEG, true><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
     else
       k_grad_limit<P, DEG, false><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
@@ -2522,6 +2555,8 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->sgeo = h.sgeo;
     t->sdx = h.sdx;
     t->fdx = h.fdx;
+    t->brick_f0 = h.brick_f0;
+    t->k1_brick = h.k1_brick;
     t->d_cperm = h.d_cperm;
     t->d_fperm = h.d_fperm;
     t->slot_geo = h.slot_geo;
@@ -2951,6 +2986,9 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
       drop_graphs(*h);
     } else if (n == "k1_tile") {
       h->k1_tile = (int)value;
+      drop_graphs(*h);
+    } else if (n == "k1_brick") {
+      h->k1_brick = (int)value;
       drop_graphs(*h);
     } else if (n == "slot_n") {
       h->slot_n = value != 0;

@@ -754,6 +754,31 @@ def test_k1_brick_path_bitwise(cid, scale, iters, gpu):
     np.testing.assert_array_equal(w, out[0][0][0])
 
 
+@pytest.mark.parametrize("cid,scale,iters", [(1, 2, 6), (2, 5, 4), (4, 20, 3), (3, 10, 3)])
+def test_k1_bulk_brick_kernel_bitwise(cid, scale, iters, gpu):
+    """The identity-phase K1 whose brick streams arrive by bulk copies
+    (k_grad_limit_brick: cp.async.bulk + mbarrier, per-face geometry windows
+    in shared memory, generic-pointer fallback outside the brick) is bitwise
+    the per-cell kernel: state, gradients and level lists, with a tail brick
+    (cell counts that are no multiple of 128) and faces outside the window."""
+    cfg = configs.get(cid, scale)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    out = {}
+    for brick in (0, 1):
+        g = Solver(mesh, "euler")
+        g.set_flag("k1_tile", 0)
+        g.set_flag("k1_brick", brick)
+        g.set_state(w0)
+        recs = g.reference_integrate(cfg.options(), iters)
+        out[brick] = (g.get_state(), g.get_array("grad"), [r["level_cells"] for r in recs])
+        g.close()
+    np.testing.assert_array_equal(out[0][0][0], out[1][0][0])
+    np.testing.assert_array_equal(out[0][0][1], out[1][0][1])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
 @pytest.mark.parametrize("cid,scale,world,iters", [(3, 10, 3, 3), (4, 20, 2, 2)])
 def test_window_slab_shards_bitwise(cid, scale, world, iters, gpu):
     """Per-rank slab windows (shard.slab_window: each rank generates only its

@@ -21,6 +21,7 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--iters", type=int, default=1)
 ap.add_argument("--graph", type=int, default=1, help="0: direct launches (per-kernel ncu ids are stable)")
+ap.add_argument("--flag", action="append", default=[], help="library knob name=value")
 a = ap.parse_args()
 cfg = configs.get(a.config)
 mesh = cfg.mesh()
@@ -28,6 +29,9 @@ s = Solver(mesh, "euler")
 s.set_state(cfg.initial_state(mesh))
 del mesh
 s.set_flag("use_graph", a.graph)
+for fv in a.flag:
+    k, v = fv.split("=")
+    s.set_flag(k, int(v))
 opt = cfg.options()
 s.reference_integrate(opt, a.warmup)
 torch.cuda.synchronize()
