@@ -63,8 +63,20 @@ struct MeshDev {
   // fc' - c_right (fc' = the partner's centroid across a periodic link), as
   // {dLx, dLy, dLz, 0}, {dRx, dRy, dRz, 0}: the same IEEE differences the
   // kernel would form, loaded by face index instead of gathered by cell.
+  // TAFV_FDX_SPLIT: the left offsets of every face, then the right ones (a
+  // warp's load covers 8 lines instead of 16), else interleaved per face.
   const double4* __restrict__ fdx;
 };
+#ifndef TAFV_FDX_SPLIT
+#define TAFV_FDX_SPLIT 1
+#endif
+#if TAFV_FDX_SPLIT
+#define TAFV_FDX_L(f, F) ((size_t)(f))
+#define TAFV_FDX_R(f, F) ((size_t)(F) + (size_t)(f))
+#else
+#define TAFV_FDX_L(f, F) (2 * (size_t)(f))
+#define TAFV_FDX_R(f, F) (2 * (size_t)(f) + 1)
+#endif
 
 struct StateDev {
   double* w;     // [N][NV] committed intensive
@@ -125,23 +137,64 @@ struct PlanDev {
 // is loaded together with tau, so the common case costs one dependent load,
 // not two; a cell straddling the front then loads its other row and
 // interpolates. Returns tau.
-template <int NV>
-__device__ __forceinline__ int stage_spec(const StateDev& s, int x, int front, bool pred, double* out) {
-  const double* base = (pred ? s.w : s.wp) + (size_t)x * NV;
+// A cell's state row (NV doubles at arr + x NV). With an odd NV >= 3 (Euler:
+// 40-byte rows) the row starts on a 16-byte boundary for even x and 8 bytes
+// past one for odd x: WIDE loads the (NV + 1) / 2 aligned 16-byte pairs that
+// cover it (one double before the row for odd x, one past it for even x; the
+// state arrays are allocated with that slack) and selects, so a warp's row
+// load is 3 instructions of 3 L1 wavefronts per line touched instead of 5
+// (K2 runs at ~80 % of the L1 data pipe; profiles/r2_k2_l1.md).
+#ifndef TAFV_ROW128
+#define TAFV_ROW128 1  // 0 off, 1 K2, 2 K2 and K1
+#endif
+template <int NV, bool WIDE>
+__device__ __forceinline__ void load_row(const double* __restrict__ arr, int x, double* out) {
+  if constexpr (WIDE && NV >= 3 && (NV & 1)) {
+    const size_t e0 = (size_t)x * NV;
+    const bool odd = e0 & 1;
+    const double2* p = reinterpret_cast<const double2*>(arr + (e0 & ~(size_t)1));
+    double v[NV + 1];
 #pragma unroll
-  for (int k = 0; k < NV; ++k) out[k] = __ldg(base + k);
+    for (int q = 0; q < (NV + 1) / 2; ++q) {
+      const double2 t = __ldg(p + q);
+      v[2 * q] = t.x;
+      v[2 * q + 1] = t.y;
+    }
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = odd ? v[k + 1] : v[k];
+  } else {
+    const double* base = arr + (size_t)x * NV;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = __ldg(base + k);
+  }
+}
+
+template <int NV, bool WIDE = false>
+__device__ __forceinline__ int stage_spec(const StateDev& s, int x, int front, bool pred, double* out) {
+  load_row<NV, WIDE>(pred ? s.w : s.wp, x, out);
   const int tx = __ldg(s.tau + x);
   const int win = 1 << tx;
   const int off = front & (win - 1);
   if (off != 0) {
     const double th = (double)off / (double)win;
-    const double* other = (pred ? s.wp : s.w) + (size_t)x * NV;
+    if constexpr (WIDE && NV >= 3 && (NV & 1)) {
+      double o[NV];
+      load_row<NV, true>(pred ? s.wp : s.w, x, o);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const double o = __ldg(other + k);
-      const double a = pred ? out[k] : o;   // w
-      const double b = pred ? o : out[k];   // w_pred
-      out[k] = a + th * (b - a);
+      for (int k = 0; k < NV; ++k) {
+        const double a = pred ? out[k] : o[k];   // w
+        const double b = pred ? o[k] : out[k];   // w_pred
+        out[k] = a + th * (b - a);
+      }
+    } else {
+      const double* other = (pred ? s.wp : s.w) + (size_t)x * NV;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const double o = __ldg(other + k);
+        const double a = pred ? out[k] : o;   // w
+        const double b = pred ? o : out[k];   // w_pred
+        out[k] = a + th * (b - a);
+      }
     }
   }
   return tx;
@@ -340,7 +393,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #pragma unroll
           for (int k = 0; k < NV; ++k) wn[k] = srow[(nb - lo) * NV + k];
         } else {
-          stage_spec<NV>(s, nb, front, pred, wn);
+          stage_spec<NV, (TAFV_ROW128 >= 2)>(s, nb, front, pred, wn);
         }
 #endif
 #pragma unroll
@@ -455,7 +508,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       double we[NV];
       if (ii < n) {
         c = base + (rev ? n - 1 - ii : ii);
-        stage_spec<NV>(s, c, front, pred, we);
+        stage_spec<NV, (TAFV_ROW128 >= 2)>(s, c, front, pred, we);
 #pragma unroll
         for (int k = 0; k < NV; ++k) srow[(c - lo) * NV + k] = we[k];
       }
@@ -479,7 +532,7 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
       const int i = rev ? n - 1 - ii : ii;
       const int c = list ? list[i] : base + i;
       double we[NV];
-      stage_spec<NV>(s, c, front, pred, we);
+      stage_spec<NV, (TAFV_ROW128 >= 2)>(s, c, front, pred, we);
       cell(c, we, 0, 0, nullptr, nullptr, nullptr, 0);
     }
   }
@@ -766,11 +819,11 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     int tl;
     {
       double we[NV];
-      tl = stage_spec<NV>(s, lr.x, front, PRED, we);
+      tl = stage_spec<NV, (TAFV_ROW128 >= 1)>(s, lr.x, front, PRED, we);
       double g[GradRow<NV>::S];
       load_grad<NV>(s, lr.x, g);
       if (m.fdx) {
-        const double4 a = ld4(m.fdx + 2 * (size_t)f);
+        const double4 a = ld4(m.fdx + TAFV_FDX_L(f, m.n_faces));
         const double dl[3] = {a.x, a.y, a.z};
 #pragma unroll
         for (int k = 0; k < NV; ++k) wL[k] = extrapolate_d<D>(we[k], g + 3 * k, dl);
@@ -789,13 +842,13 @@ __global__ void __launch_bounds__(128, TAFV_K2_MINB) k_face_flux(MeshDev m, Stat
     bool eq = true;  // equal-level (or boundary) face
     if (lr.y >= 0) {
       double we[NV];
-      const int tr = stage_spec<NV>(s, lr.y, front, PRED, we);
+      const int tr = stage_spec<NV, (TAFV_ROW128 >= 1)>(s, lr.y, front, PRED, we);
       eq = tr == tl;
       shared_start = shared_start && (front & ((1 << tr) - 1)) == 0;
       double g[GradRow<NV>::S];
       load_grad<NV>(s, lr.y, g);
       if (m.fdx) {
-        const double4 b = ld4(m.fdx + 2 * (size_t)f + 1);
+        const double4 b = ld4(m.fdx + TAFV_FDX_R(f, m.n_faces));
         const double dr[3] = {b.x, b.y, b.z};
 #pragma unroll
         for (int k = 0; k < NV; ++k) wR[k] = extrapolate_d<D>(we[k], g + 3 * k, dr);

@@ -255,8 +255,8 @@ __global__ void k_face_dx(const int2* lr, const int* rcf, const double* fcen, co
       const int t = periodic ? rcf[j] : j;
       for (int d = 0; d < 3; ++d) dr[d] = fcen[3 * (size_t)t + d] - cen[3 * (size_t)r + d];
     }
-    fdx[2 * (size_t)j] = make_double4(dl[0], dl[1], dl[2], 0.0);
-    fdx[2 * (size_t)j + 1] = make_double4(dr[0], dr[1], dr[2], 0.0);
+    fdx[TAFV_FDX_L(j, F)] = make_double4(dl[0], dl[1], dl[2], 0.0);
+    fdx[TAFV_FDX_R(j, F)] = make_double4(dr[0], dr[1], dr[2], 0.0);
   }
 }
 

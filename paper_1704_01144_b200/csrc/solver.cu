@@ -755,8 +755,8 @@ void upload_mesh_host(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls 
         const int t = h.periodic ? rcf[j] : j;
         for (int d = 0; d < 3; ++d) dr[d] = fcen[3 * (size_t)t + d] - cen[3 * (size_t)r + d];
       }
-      fdx[2 * (size_t)j] = make_double4(dl[0], dl[1], dl[2], 0.0);
-      fdx[2 * (size_t)j + 1] = make_double4(dr[0], dr[1], dr[2], 0.0);
+      fdx[TAFV_FDX_L(j, F)] = make_double4(dl[0], dl[1], dl[2], 0.0);
+      fdx[TAFV_FDX_R(j, F)] = make_double4(dr[0], dr[1], dr[2], 0.0);
     }
     h.fdx = dalloc<double4>(2 * (size_t)F);
     up(h.fdx, fdx);
@@ -1048,9 +1048,10 @@ void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nul
 
 void alloc_state(tafv_gpu& h) {
   const size_t N = h.N, F = h.F, nv = h.nv;
-  h.w = dalloc<double>(N * nv);
-  h.W = dalloc<double>(N * nv);
-  h.wp = dalloc<double>(N * nv);
+  // + 2: load_row's aligned 16-byte pairs reach one double past the last row
+  h.w = dalloc<double>(N * nv + 2);
+  h.W = dalloc<double>(N * nv + 2);
+  h.wp = dalloc<double>(N * nv + 2);
   h.gs = (nv * 3 + 3) / 4 * 4;  // GradRow<NV>::S
   h.grad = dalloc<double>(N * h.gs);
   h.fs = (nv + 1) / 2 * 2;  // FaceRow<NV>::S
