@@ -24,7 +24,10 @@
 // Threading: every kernel is a pure per-item loop (kernels.hpp:12-21), so the
 // item list is split into contiguous chunks over a small thread pool, the
 // same shape as the reference's LaneGang (runtime.cpp:16-79). Results are
-// bitwise independent of the thread count.
+// bitwise independent of the thread count. A second driver (TaskDriver, below)
+// runs the same kernels as per-CE tasks with declared data accesses on a
+// sequential-task-flow runtime, the shape of the reference's TaskEngine
+// (taskgen.cpp:348-661), as a timed CPU baseline; bitwise the same state.
 // ============================================================================
 
 #include <algorithm>
@@ -33,15 +36,19 @@
 #include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <exception>
 #include <functional>
 #include <limits>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 namespace oracle {
@@ -986,6 +993,419 @@ struct Driver {
   }
 };
 
+// --- the task-shaped driver (the reference's STF engine shape) ----------------
+// CPU baseline only: the same Euler / scalar kernels
+// driven the way TaskEngine::run_iteration drives the reference's
+// (taskgen.cpp:348-523, 525-661): the mesh is cut into computational elements
+// (CEs; ce.cpp:19-64 -- here equal chunks of the id or a Morton order), each CE's cells are split
+// into inner cells (every neighbour in the CE) and border cells, its faces into
+// intra-CE faces and inter-CE pair groups, all binned by level; every phase is
+// emitted as the reference's four passes of per-CE tasks -- (0) stage border
+// cells, (1) stage inner, gradient + limiter inner, then border, (2) window
+// reset / reconstruction / Riemann on intra faces and on pair groups, (3) flux
+// sums and updates, inner then border -- whose data accesses on four kinds of
+// handles (inner[ce], border[ce], faces[ce], pair[a,b]) are declared read or
+// write, and a sequential-task-flow runtime (runtime.cpp's model: a task waits
+// for the last writer of what it reads, and for every reader since the last
+// writer of what it writes) runs them on worker threads with NO barrier between
+// kernels, phases or subiterations. Every kernel call is the barrier driver's,
+// on a CE's item list, so the state is bitwise the sequential driver's; only
+// the ledger's compensated sum takes its terms in (phase, CE) order.
+struct TaskGraph {
+  struct Task {
+    std::function<void()> fn;
+    std::vector<int> succ;
+    int ndeps = 0;
+  };
+  struct Handle {
+    int last_writer = -1;
+    std::vector<int> readers;
+  };
+  std::vector<Task> tasks;
+  std::vector<Handle> handles;
+
+  explicit TaskGraph(int nhandles) : handles(nhandles) {}
+
+  void add(std::function<void()> fn, const std::vector<int>& reads, const std::vector<int>& writes) {
+    const int id = static_cast<int>(tasks.size());
+    std::vector<int> deps;
+    for (int h : reads) {
+      if (handles[h].last_writer >= 0) deps.push_back(handles[h].last_writer);
+      handles[h].readers.push_back(id);
+    }
+    for (int h : writes) {
+      Handle& hd = handles[h];
+      if (hd.last_writer >= 0) deps.push_back(hd.last_writer);
+      for (int r : hd.readers)
+        if (r != id) deps.push_back(r);
+      hd.last_writer = id;
+      hd.readers.clear();
+    }
+    std::sort(deps.begin(), deps.end());
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    tasks.emplace_back();
+    tasks.back().fn = std::move(fn);
+    tasks.back().ndeps = static_cast<int>(deps.size());
+    for (int d : deps) tasks[d].succ.push_back(id);
+  }
+
+  void run(int threads) {
+    const int n = static_cast<int>(tasks.size());
+    std::vector<int> left(n);
+    std::deque<int> ready;
+    for (int i = 0; i < n; ++i) {
+      left[i] = tasks[i].ndeps;
+      if (left[i] == 0) ready.push_back(i);
+    }
+    std::mutex mu;
+    std::condition_variable cv;
+    int done = 0;
+    std::exception_ptr err;
+    auto worker = [&] {
+      std::unique_lock<std::mutex> lk(mu);
+      for (;;) {
+        cv.wait(lk, [&] { return !ready.empty() || done == n || err; });
+        if (done == n || err) return;
+        const int t = ready.front();
+        ready.pop_front();
+        lk.unlock();
+        std::exception_ptr e;
+        try {
+          tasks[t].fn();
+        } catch (...) {
+          e = std::current_exception();
+        }
+        lk.lock();
+        if (e && !err) err = e;
+        ++done;
+        int woke = 0;
+        for (int sidx : tasks[t].succ)
+          if (--left[sidx] == 0) {
+            ready.push_back(sidx);
+            ++woke;
+          }
+        if (done == n || err) cv.notify_all();
+        else if (woke > 1) cv.notify_all();
+        else if (woke == 1) cv.notify_one();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    if (err) std::rethrow_exception(err);
+  }
+};
+
+// The CE decomposition of a mesh (static: ce.cpp:19-90's role): compact
+// equal-size CEs; a cell is a border cell when a neighbour lies in another CE; a face
+// belongs to its CE (both sides inside, or a boundary face) or to the pair of
+// CEs it joins.
+struct CeDecomp {
+  int n_ce = 1, chunk = 1;
+  std::vector<int> ce_id;  // cell -> CE
+  std::vector<uint8_t> is_border;
+  std::vector<std::vector<int>> inner_raw, border_raw, intra_raw, pair_raw;
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<std::vector<int>> ce_pairs, ce_nbrs;
+};
+inline std::shared_ptr<CeDecomp> build_decomp(const Mesh& m, int nce_signed, Pool& pool) {
+  auto dc = std::make_shared<CeDecomp>();
+  const int nce = std::abs(nce_signed);
+  const int n_ce = dc->n_ce = std::max(1, std::min(nce, m.nc));
+  const int chunk = dc->chunk = (m.nc + n_ce - 1) / n_ce;
+  dc->ce_id.resize(m.nc);
+  if (nce_signed > 0) {
+    // equal chunks of the id order: on a lattice-ordered mesh these are sheets
+    // across the graded direction, so every CE holds its share of every level
+    // (the level-cost balance DistDriver::repartition aims at, exchange.cpp:598-603)
+    for (int c = 0; c < m.nc; ++c) dc->ce_id[c] = c / chunk;
+  } else {
+    // compact CEs (the role of partition.cpp's region growing): equal chunks of
+    // the cells in Morton order of their centroids
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) lo[a] = hi[a] = m.cen[a];
+    for (int c = 0; c < m.nc; ++c)
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], m.cen[3 * static_cast<size_t>(c) + a]);
+        hi[a] = std::max(hi[a], m.cen[3 * static_cast<size_t>(c) + a]);
+      }
+    // one scale for every axis, so that the curve's cells are cubes in space
+    double ext = 0.0;
+    for (int a = 0; a < 3; ++a) ext = std::max(ext, hi[a] - lo[a]);
+    const double scale = ext > 0.0 ? 1048575.0 / ext : 0.0;
+    auto spread = [](uint64_t v) {
+      v &= 0x1fffffull;
+      v = (v | v << 32) & 0x1f00000000ffffull;
+      v = (v | v << 16) & 0x1f0000ff0000ffull;
+      v = (v | v << 8) & 0x100f00f00f00f00full;
+      v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+      v = (v | v << 2) & 0x1249249249249249ull;
+      return v;
+    };
+    std::vector<std::pair<uint64_t, int>> key(m.nc);
+    pool.run(m.nc, [&](int64_t b, int64_t e) {
+      for (int64_t c = b; c < e; ++c) {
+        uint64_t k = 0;
+        for (int a = 0; a < 3; ++a)
+          k |= spread(static_cast<uint64_t>((m.cen[3 * c + a] - lo[a]) * scale)) << a;
+        key[c] = {k, static_cast<int>(c)};
+      }
+    });
+    std::sort(key.begin(), key.end());
+    for (int i = 0; i < m.nc; ++i) dc->ce_id[key[i].second] = i / chunk;
+  }
+  auto ce_of = [&](int c) { return dc->ce_id[c]; };
+  dc->is_border.assign(m.nc, 0);
+  pool.run(m.nc, [&](int64_t b, int64_t e) {
+    for (int64_t c = b; c < e; ++c)
+      for (int t = m.adj_off[c]; t < m.adj_off[c + 1]; ++t) {
+        const int nb = m.adj_nb[t];
+        if (nb >= 0 && ce_of(nb) != ce_of(static_cast<int>(c))) dc->is_border[c] = 1;
+      }
+  });
+  dc->inner_raw.resize(n_ce);
+  dc->border_raw.resize(n_ce);
+  dc->intra_raw.resize(n_ce);
+  for (int c = 0; c < m.nc; ++c) (dc->is_border[c] ? dc->border_raw : dc->inner_raw)[ce_of(c)].push_back(c);
+  std::map<std::pair<int, int>, int> pair_index;
+  for (int f = 0; f < m.nf; ++f) {
+    const int a = ce_of(m.fl[f]);
+    const int r = m.resolved_right(f);
+    const int b = r >= 0 ? ce_of(r) : a;
+    if (a == b) {
+      dc->intra_raw[a].push_back(f);
+    } else {
+      const std::pair<int, int> key{std::min(a, b), std::max(a, b)};
+      auto it = pair_index.find(key);
+      if (it == pair_index.end()) {
+        it = pair_index.emplace(key, static_cast<int>(dc->pairs.size())).first;
+        dc->pairs.push_back(key);
+        dc->pair_raw.emplace_back();
+      }
+      dc->pair_raw[it->second].push_back(f);
+    }
+  }
+  dc->ce_pairs.resize(n_ce);
+  dc->ce_nbrs.resize(n_ce);
+  for (int q = 0; q < static_cast<int>(dc->pairs.size()); ++q) {
+    dc->ce_pairs[dc->pairs[q].first].push_back(q);
+    dc->ce_pairs[dc->pairs[q].second].push_back(q);
+    dc->ce_nbrs[dc->pairs[q].first].push_back(dc->pairs[q].second);
+    dc->ce_nbrs[dc->pairs[q].second].push_back(dc->pairs[q].first);
+  }
+  return dc;
+}
+
+template <class P>
+struct TaskDriver {
+  Driver<P>& d;
+  const CeDecomp& decomp;
+  Pool serial{1};
+  Kernels<P> ks{d.m, d.st, d.ph, serial};
+
+  // Items of one iteration (taskgen.cpp build_iteration_items): per CE the
+  // cells sorted by level (prefix = "tau <= l"), inner and border apart; intra
+  // faces and pair groups sorted by cadence; the fringe lists split likewise.
+  struct Sorted {
+    std::vector<int> items;
+    std::vector<int> upto;  // upto[l] = |{items : level <= l}|
+    const int* data() const { return items.data(); }
+    int64_t count(int level) const { return upto.empty() ? 0 : upto[std::min<size_t>(level, upto.size() - 1)]; }
+  };
+  static Sorted sort_by_level(const std::vector<int>& items, const std::vector<int>& level_of, int theta) {
+    Sorted s;
+    s.upto.assign(theta + 1, 0);
+    for (int x : items) ++s.upto[level_of[x]];
+    std::vector<int> at(theta + 1, 0);
+    for (int l = 1; l <= theta; ++l) at[l] = at[l - 1] + s.upto[l - 1];
+    s.items.resize(items.size());
+    std::vector<int> cur = at;
+    for (int x : items) s.items[cur[level_of[x]]++] = x;
+    for (int l = 0; l <= theta; ++l) s.upto[l] = cur[l];
+    return s;
+  }
+
+  Record run_iteration(const IterationPlan& plan, int threads) {
+    const Mesh& m = d.m;
+    State& st = d.st;
+    const int theta = plan.theta();
+    const double dt = plan.levels.dt;
+    const std::vector<int>& tau = plan.levels.tau;
+    const std::vector<int>& cad = plan.face_cadence;
+    const CeDecomp& dc = decomp;
+    const int n_ce = dc.n_ce;
+    auto ce_of = [&](int c) { return dc.ce_id[c]; };
+    const std::vector<uint8_t>& is_border = dc.is_border;
+    const auto& inner_raw = dc.inner_raw;
+    const auto& border_raw = dc.border_raw;
+    const auto& intra_raw = dc.intra_raw;
+    const auto& pair_raw = dc.pair_raw;
+    const auto& pairs = dc.pairs;
+    const auto& ce_pairs = dc.ce_pairs;
+    const auto& ce_nbrs = dc.ce_nbrs;
+    const int n_pair = static_cast<int>(pairs.size());
+    std::vector<Sorted> inner(n_ce), border(n_ce), intra(n_ce), pfaces(n_pair);
+    d.pool.run(n_ce, [&](int64_t b, int64_t e) {
+      for (int64_t q = b; q < e; ++q) {
+        inner[q] = sort_by_level(inner_raw[q], tau, theta);
+        border[q] = sort_by_level(border_raw[q], tau, theta);
+        intra[q] = sort_by_level(intra_raw[q], cad, theta);
+      }
+    });
+    d.pool.run(n_pair, [&](int64_t b, int64_t e) {
+      for (int64_t q = b; q < e; ++q) pfaces[q] = sort_by_level(pair_raw[q], cad, theta);
+    });
+    // fringe[level] split by CE and class
+    std::vector<std::vector<std::vector<int>>> fr_in(theta), fr_bd(theta);
+    for (int l = 0; l < theta; ++l) {
+      fr_in[l].resize(n_ce);
+      fr_bd[l].resize(n_ce);
+      for (int c : plan.fringe[l]) (is_border[c] ? fr_bd[l] : fr_in[l])[ce_of(c)].push_back(c);
+    }
+
+    // --- handles and the ledger's partial sums
+    auto h_inner = [&](int q) { return q; };
+    auto h_border = [&](int q) { return n_ce + q; };
+    auto h_faces = [&](int q) { return 2 * n_ce + q; };
+    auto h_pair = [&](int q) { return 3 * n_ce + q; };
+    TaskGraph g(3 * n_ce + n_pair);
+    const int subiterations = plan.subiterations();
+    const int n_corr = subiterations;  // correctors: subiterations - 1 inside the sweep + the trailing one
+    std::vector<double> led(static_cast<size_t>(n_corr) * n_ce * 2 * P::NV, 0.0);
+
+    const double t_start = st.t0;
+    reset_fronts(st);
+    int corr_index = 0;
+    const std::vector<int> none;  // outlives the tasks that hold a reference to it
+    auto emit_phase = [&](bool corr, int level, int front, int ci) {
+      const int phase = corr ? kCorrector : kPredictor;
+      // pass 0: border cells staged first (taskgen.cpp:360-383)
+      for (int q = 0; q < n_ce; ++q) {
+        const int64_t nb = border[q].count(level);
+        const std::vector<int>& fb = level < theta ? fr_bd[level][q] : none;
+        if (nb == 0 && fb.empty()) continue;
+        g.add([this, &tau, &border, &fb, q, nb, front, corr, phase] {
+          if (corr) ks.stage_predicted(tau, border[q].data(), nb, front);
+          else ks.stage_committed(border[q].data(), nb, front);
+          ks.stage_interpolated(tau, fb.data(), fb.size(), front, phase);
+        }, {}, {h_border(q)});
+      }
+      // pass 1: inner staging, gradients and limiter inner, then border (:385-421)
+      for (int q = 0; q < n_ce; ++q) {
+        const int64_t ni = inner[q].count(level), nb = border[q].count(level);
+        const std::vector<int>& fi = level < theta ? fr_in[level][q] : none;
+        if (ni > 0 || !fi.empty())
+          g.add([this, &tau, &inner, &fi, q, ni, front, corr, phase] {
+            if (corr) ks.stage_predicted(tau, inner[q].data(), ni, front);
+            else ks.stage_committed(inner[q].data(), ni, front);
+            ks.stage_interpolated(tau, fi.data(), fi.size(), front, phase);
+          }, {}, {h_inner(q)});
+        if (ni > 0)
+          g.add([this, &inner, q, ni, front, phase] {
+            ks.green_gauss_gradient(inner[q].data(), ni, front, phase);
+            ks.limit_gradients(inner[q].data(), ni, front, phase);
+          }, {h_border(q)}, {h_inner(q)});
+        if (nb > 0) {
+          std::vector<int> reads{h_inner(q)};
+          for (int o : ce_nbrs[q]) reads.push_back(h_border(o));
+          g.add([this, &border, q, nb, front, phase] {
+            ks.green_gauss_gradient(border[q].data(), nb, front, phase);
+            ks.limit_gradients(border[q].data(), nb, front, phase);
+          }, reads, {h_border(q)});
+        }
+      }
+      // pass 2: faces -- intra-CE, then the pair groups, emitted once (:423-474)
+      for (int q = 0; q < n_ce; ++q) {
+        const int64_t nf = intra[q].count(level);
+        if (nf == 0) continue;
+        double* part = corr ? &led[(static_cast<size_t>(ci) * n_ce + q) * 2 * P::NV] : nullptr;
+        g.add([this, &cad, &intra, q, nf, front, corr, phase, dt, part] {
+          const int* f = intra[q].data();
+          if (!corr) ks.reset_windows(f, nf, front);
+          ks.reconstruct_faces(f, nf, front, phase);
+          if (corr) {
+            ks.riemann_correct(cad, dt, f, nf, front);
+            for (int64_t i = 0; i < nf; ++i) {  // the ledger's terms of this CE and phase
+              if (d.m.resolved_right(f[i]) >= 0) continue;
+              for (int k = 0; k < P::NV; ++k) {
+                const double b = d.st.int_substep[f[i] * P::NV + k];
+                const double sum = part[k] + b, bb = sum - part[k];
+                part[P::NV + k] += (part[k] - (sum - bb)) + (b - bb);
+                part[k] = sum;
+              }
+            }
+          } else {
+            ks.riemann_predict(f, nf, front);
+          }
+        }, {h_inner(q), h_border(q)}, {h_faces(q)});
+      }
+      for (int q = 0; q < n_pair; ++q) {
+        const int64_t nf = pfaces[q].count(level);
+        if (nf == 0) continue;
+        g.add([this, &cad, &pfaces, q, nf, front, corr, phase, dt] {
+          const int* f = pfaces[q].data();
+          if (!corr) ks.reset_windows(f, nf, front);
+          ks.reconstruct_faces(f, nf, front, phase);
+          if (corr) ks.riemann_correct(cad, dt, f, nf, front);
+          else ks.riemann_predict(f, nf, front);
+        }, {h_border(pairs[q].first), h_border(pairs[q].second)}, {h_pair(q)});
+      }
+      // pass 3: flux sums and updates, inner then border (:476-513)
+      for (int q = 0; q < n_ce; ++q) {
+        const int64_t ni = inner[q].count(level), nb = border[q].count(level);
+        auto update = [this, &tau, &cad, front, corr, dt](const int* c, int64_t n) {
+          if (corr) {
+            ks.flux_sum_correct(tau, cad, c, n, front);
+            ks.extensive_correct(c, n);
+            ks.intensive_correct(tau, c, n, front);
+          } else {
+            ks.flux_sum_predict(c, n, front);
+            ks.extensive_predict(tau, dt, c, n);
+            ks.intensive_predict(c, n);
+          }
+        };
+        if (ni > 0)
+          g.add([&inner, q, ni, update] { update(inner[q].data(), ni); }, {h_faces(q)}, {h_inner(q)});
+        if (nb > 0) {
+          std::vector<int> reads{h_faces(q)};
+          for (int pq : ce_pairs[q]) reads.push_back(h_pair(pq));
+          g.add([&border, q, nb, update] { update(border[q].data(), nb); }, reads, {h_border(q)});
+        }
+      }
+    };
+    // the phase order of run_iteration (reference.cpp:100-129)
+    for (int s = 1; s <= subiterations; ++s) {
+      const int level = subiteration_level(s, theta);
+      const int front = s - 1;
+      if (s > 1) emit_phase(true, level, front, corr_index++);
+      emit_phase(false, level, front, -1);
+    }
+    emit_phase(true, theta, subiterations, corr_index++);
+    n_tasks = static_cast<int64_t>(g.tasks.size());
+    g.run(threads);
+
+    // ledger: the partials in (phase, CE) order, compensated
+    for (int k = 0; k < 8; ++k) d.bflux[k] = d.bcomp[k] = 0.0;
+    for (size_t i = 0; i < led.size() / (2 * P::NV); ++i)
+      for (int k = 0; k < P::NV; ++k)
+        for (int part = 0; part < 2; ++part) {
+          const double b = led[i * 2 * P::NV + part * P::NV + k];
+          const double sum = d.bflux[k] + b, bb = sum - d.bflux[k];
+          d.bcomp[k] += (d.bflux[k] - (sum - bb)) + (b - bb);
+          d.bflux[k] = sum;
+        }
+    const Items all_cells = iota_items(m.nc);
+    if (!d.k.finite_state(all_cells.data(), m.nc))
+      throw std::runtime_error("integrate: solution diverged to a non-finite state");
+    d.k.finalize_cells(all_cells.data(), m.nc);
+    st.t0 = t_start + dt * static_cast<double>(subiterations);
+    st.iteration += 1;
+    return d.make_record(plan, t_start);
+  }
+  int64_t n_tasks = 0;
+};
+
 // --- type-erased solver -------------------------------------------------------
 enum Model { kAdvection = 0, kBurgers = 1, kEuler = 2 };
 
@@ -1001,6 +1421,8 @@ struct Solver {
   IterationPlan plan;
   bool has_plan = false;
   std::unique_ptr<Pool> pool = std::make_unique<Pool>(1);
+  std::shared_ptr<CeDecomp> decomp;  // task driver: the CE decomposition of the last n_ce
+  int decomp_nce = 0;
 };
 
 template <class F>
@@ -1282,6 +1704,32 @@ int orc_integrate(void* sp, int n, Record* recs) {  // reference.cpp:131-142
       s->plan = with_physics(*s, [&](auto& d) { return d.plan_iteration(s->opt); });
       s->has_plan = true;
       recs[i] = with_physics(*s, [&](auto& d) { return d.run_iteration(s->plan); });
+    }
+  });
+}
+
+// reference_integrate with run_iteration through the task-shaped driver
+// (TaskEngine::integrate, taskgen.cpp:663-672): n_ce computational elements,
+// the solver's thread count as workers. tasks_out: tasks of the last iteration.
+int orc_integrate_tasks(void* sp, int n, int n_ce, int threads, Record* recs, int64_t* tasks_out) {
+  return guard([&] {
+    auto* s = static_cast<Solver*>(sp);
+    require(n >= 0, "integrate: negative iteration count");
+    require(n_ce != 0 && threads >= 1, "integrate_tasks: n_ce must be non-zero and threads positive");
+    if (!s->decomp || s->decomp_nce != n_ce) {
+      s->decomp = build_decomp(*s->m, n_ce, *s->pool);
+      s->decomp_nce = n_ce;
+    }
+    for (int i = 0; i < n; ++i) {
+      s->plan = with_physics(*s, [&](auto& d) { return d.plan_iteration(s->opt); });
+      s->has_plan = true;
+      recs[i] = with_physics(*s, [&](auto& d) {
+        using PH = std::remove_cv_t<std::remove_reference_t<decltype(d.ph)>>;
+        TaskDriver<PH> td{d, *s->decomp};
+        Record r = td.run_iteration(s->plan, threads);
+        if (tasks_out) *tasks_out = td.n_tasks;
+        return r;
+      });
     }
   });
 }

@@ -55,6 +55,11 @@ def test_reference_arm_line_contract():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     s1 = d["cpu_single_thread"]
     assert s1["cores"] == 1 and s1["value"] > 0
+    # the task-shaped leg ran on the same sample; the line's value is the faster driver's
+    ts, bp = d["cpu_task_shape"], d["cpu_barrier_pool"]
+    if cb["cores"] > 1:
+        assert ts["value"] > 0 and ts["ces"] == 4 * ts["cores"] and ts["tasks_per_iteration"] > 0
+        assert d["value"] == max(ts["value"], bp["value"])
     e = d["e2e"]
     assert e["value"] == d["value"] and e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
 

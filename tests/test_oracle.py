@@ -412,6 +412,59 @@ def test_oracle_threading_is_bitwise_invariant():
     assert np.array_equal(out[0], out[1])
 
 
+@pytest.mark.parametrize("cfgid,scale,iters,n_ce,threads", [(2, 6, 3, 7, 4), (4, 24, 3, 16, 8), (3, 20, 3, 1, 2),
+                                                            (1, 4, 4, 64, 3), (4, 24, 3, -12, 4),
+                                                            (2, 6, 3, -40, 8)])
+def test_oracle_task_driver_is_bitwise_the_barrier_driver(cfgid, scale, iters, n_ce, threads):
+    """The oracle's Euler kernels through the task-shaped driver (per-CE
+    tasks with declared accesses, no barriers: the shape of
+    TaskEngine::run_iteration, taskgen.cpp:525-661) leave bitwise the state and
+    the records of the barrier driver (test_taskgen.cpp's engine-vs-reference
+    property); the ledger's sum differs in order only. n_ce < 0: compact
+    (Morton) CEs instead of chunks of the id order."""
+    from paper_1704_01144_b200 import configs
+    cfg = configs.get(cfgid, scale)
+    m = cfg.mesh()
+    w0 = cfg.initial_state(m)
+    a = OracleSolver(m, "euler", threads=2)
+    b = OracleSolver(m, "euler", threads=2)
+    for o in (a, b):
+        o.init_values(w0.reshape(-1))
+        o.set_options(cfg.theta_max, cfg.cfl, cfg.dt_cap)
+    ra = a.integrate(iters)
+    rb = b.integrate_tasks(iters, n_ce, threads)
+    assert b.last_task_count > 0
+    for k in ("w", "W", "w_pred", "phi_pred", "int_substep", "int_window"):
+        assert a.get(k).tobytes() == b.get(k).tobytes(), k
+    for x, y in zip(ra, rb):
+        for key in ("dt", "theta", "level_cells", "total_extensive", "cost_ratio", "t_start", "advance"):
+            assert x[key] == y[key], key
+        scale_w = max(abs(v) for v in x["total_extensive"])
+        for u, v in zip(x["boundary_flux"], y["boundary_flux"]):
+            assert abs(u - v) <= max(1e-12 * abs(u), 1e-15 * scale_w)
+
+
+@needs_ref
+def test_oracle_task_driver_scalar_vs_reference_task_engine():
+    """Scalar 2D with periodic links and three levels: the oracle's task
+    driver, the reference's TaskEngine and the reference's sequential driver
+    agree bitwise."""
+    spec = dict(dim=2, nx=40, ny=32, periodic_x=True, periodic_y=True, regions=[((0.25, 0.25, 0.75, 0.75), 2)])
+    m, _, mh = ref_generate_mesh(**spec)
+    seq, task = RefSolver(mh, "advection", (1.0, 0.5)), RefSolver(mh, "advection", (1.0, 0.5))
+    for s in (seq, task):
+        s.init_gaussian(sigma=0.15)
+        s.set_options(3, 0.5, 1.0)
+    o = OracleSolver(m, "advection", (1.0, 0.5))
+    o.set_options(3, 0.5, 1.0)
+    o.init_values(seq.get("w"))
+    rs, rt, ro = seq.integrate(4), task.task_integrate(4, 4, 16), o.integrate_tasks(4, 16, 4)
+    assert [r["dt"] for r in rs] == [r["dt"] for r in rt] == [r["dt"] for r in ro]
+    assert np.array_equal(seq.get("w"), task.get("w"))
+    assert np.array_equal(seq.get("w"), o.get("w"))
+    assert np.array_equal(seq.get("W"), o.get("W"))
+
+
 def test_euler_sod_first_order_sanity():
     """Planar Sod (config 1 shape) on the oracle: the solution stays planar
     (y/z-invariant) and the shock/contact lie between the exact-solution
