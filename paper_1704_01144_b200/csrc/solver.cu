@@ -206,6 +206,8 @@ struct tafv_gpu {
   bool led_pending = false;
   bool iwin_alias = true;
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
+  uint8_t* sweep_tile = nullptr;  // [sweep][cell tile] marks of the Jacobi sweeps (k_level_sweep)
+  int sweep_marks = 1;            // flag "sweep_marks": skip the tiles no level change can reach
   uint8_t* fflag = nullptr;
   double *dtmax = nullptr, *blockmin = nullptr;
   unsigned* dt_ticket = nullptr;  // last-block ticket of k_dt_max
@@ -357,7 +359,7 @@ struct tafv_gpu {
         if (p) cudaFree(p);
     }
     void* ptrs[] = {w,     W,        wp,       bsum,  lpart,
-                    grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb,
+                    grad, phi,   isub,     iwin,     ialias,   tau,    cad,    raw,      tmpa,    tmpb, sweep_tile,
                     fflag, dt_ticket, dtmax, blockmin, cell_counts, face_counts, clist, flist, partials, dplan,
                     stage_buf, d_send_idx, d_recv_idx, sendbuf, recvbuf, d_cinv,
                     xkey_s, xkey_r, xpos_s, xpos_r, xsorted_s, xsorted_r, xcounts,
@@ -1073,6 +1075,7 @@ void alloc_state(tafv_gpu& h) {
   h.lpart = dalloc<DD>((size_t)nv * h.nblk_led);
   h.tau = dalloc<int8_t>(N);
   h.raw = dalloc<int8_t>(N);
+  h.sweep_tile = dalloc<uint8_t>((size_t)kMaxLevels * ((N + kTile - 1) / kTile + 1));
   h.tmpa = dalloc<int8_t>(N);
   h.tmpb = dalloc<int8_t>(N);
   h.fflag = dalloc<uint8_t>(((size_t)N + 3) & ~(size_t)3);  // word-addressed by k_face_cadence
@@ -1540,26 +1543,33 @@ void plan_kernels(tafv_gpu& h, const tafv_options& opt) {
     // last (k_level_sweep). The fixpoint is min_d raw(d) + dist(c, d); a cell
     // more than theta_max hops away cannot lower raw(c) <= theta_max, so
     // theta_max sweeps reach it exactly (levels.cpp:33-51).
-    const int ntc = std::max(1, h.ntile_c), gs = h.grid_for(h.n_own, 256);
+    const int ntc = std::max(1, h.ntile_c);
     const int sweeps = std::max(1, opt.theta_max);
+    // per-sweep tile marks (k_level_sweep): sweep i + 1 only re-evaluates the
+    // tiles a level change of sweep i can reach
+    const bool marks = h.sweep_marks && sweeps > 1;
+    if (marks) CK(cudaMemsetAsync(h.sweep_tile, 0, (size_t)sweeps * ntc, h.st));
+    const int gs = marks ? ntc : h.grid_for(h.n_own, 256);
     const int8_t* src = nullptr;
     for (int i = 0; i < sweeps; ++i) {
       const bool first = i == 0, last = i == sweeps - 1;
       int8_t* dst = last ? h.tau : (i % 2 == 0 ? h.tmpa : h.tmpb);
       const int sm = opt.theta_max > 0 ? 1 : 0;
       uint8_t* clr = first ? h.fflag : nullptr;
+      const uint8_t* tp = marks && !first ? h.sweep_tile + (size_t)(i - 1) * ntc : nullptr;
+      uint8_t* tc = marks && !last ? h.sweep_tile + (size_t)i * ntc : nullptr;
       if (first && last)
         k_level_sweep<true, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0, tp, tc);
       else if (first)
         k_level_sweep<true, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
+                                                                     sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0, tp, tc);
       else if (last)
         k_level_sweep<false, true><<<ntc, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0, tp, tc);
       else
         k_level_sweep<false, false><<<gs, kCompactThreads, 0, h.st>>>(md, src, h.dtmax, h.dplan, opt.theta_max,
-                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0);
+                                                                      sm, dst, h.n_own, nkeys, h.cell_counts, clr, i, h.deg6 ? 6 : 0, tp, tc);
       ++h.launches;
       src = dst;
     }
@@ -2984,6 +2994,9 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+      drop_graphs(*h);
+    } else if (n == "sweep_marks") {
+      h->sweep_marks = value != 0;
       drop_graphs(*h);
     } else if (n == "k1_tile") {
       h->k1_tile = (int)value;

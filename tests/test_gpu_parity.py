@@ -325,6 +325,42 @@ def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, iwin_alias, gpu):
     assert [r["t_start"] for r in rg] == [r["t_start"] for r in ro]
 
 
+@pytest.mark.parametrize("cid,scale,iters", [(3, 8, 5), (4, 10, 4), (2, 4, 6)])
+def test_sweep_tile_marks_are_invisible(cid, scale, iters, gpu):
+    """The Jacobi sweeps of plan_iteration with the per-tile change marks
+    (sweep i + 1 re-evaluates only the tiles a level change of sweep i can
+    reach, the rest is copied) leave bit-exact the level map, every plan list,
+    the records and the state of the sweeps without them (levels.cpp:33-51);
+    several tiles and levels that move between iterations."""
+    cfg = configs.get(cid, scale)
+    mesh = cfg.mesh()
+    w0 = cfg.initial_state(mesh)
+    opt = cfg.options()
+    runs = []
+    for marks in (1, 0):
+        g = Solver(mesh, "euler")
+        g.set_flag("sweep_marks", marks)
+        g.set_state(w0)
+        lists, recs = [], []
+        for _ in range(iters):
+            g.plan_iteration(opt)
+            lists.append(g.plan_lists())
+            recs.append(g.run_iteration())
+        runs.append((lists, recs, g.get_state()))
+    (la, ra, sa), (lb, rb, sb) = runs
+    assert len(mesh["vol"]) > 3 * 2048  # more than one tile
+    for x, y in zip(la, lb):
+        for key in ("tau", "face_cadence"):
+            np.testing.assert_array_equal(x[key], y[key])
+        for key in ("cells_of_level", "faces_of_cadence", "fringe"):
+            for u, v in zip(x[key], y[key]):
+                np.testing.assert_array_equal(u, v)
+    assert [r["level_cells"] for r in ra] == [r["level_cells"] for r in rb]
+    assert [r["dt"] for r in ra] == [r["dt"] for r in rb]
+    assert sa[0].tobytes() == sb[0].tobytes() and sa[1].tobytes() == sb[1].tobytes()
+    assert len(set(tuple(r["level_cells"]) for r in ra)) > 1  # the level map moved
+
+
 @pytest.mark.parametrize("cid,scale", [(2, 6), (4, 8)])
 def test_window_alias_is_invisible(cid, scale, gpu):
     """Skipping int_window traffic on equal-level faces (StateDev::ialias)
