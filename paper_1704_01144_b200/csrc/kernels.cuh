@@ -1356,7 +1356,19 @@ struct CompactJob {
   long long* totals; // [kMaxLevels]
   int* prefix;       // [kMaxLevels]
   int base;
+  // or null: per-level CELL totals; the list entries of the top level theta
+  // (the highest level with cells) are not written -- every consumer takes a
+  // prefix "key <= l" with l < theta, the phases at level theta run over the
+  // identity range (single domain only)
+  const long long* top_of;
 };
+__device__ __forceinline__ int skipped_key(const CompactJob& jb, int nkeys) {
+  int top = -1;
+  if (jb.top_of)
+    for (int k = 0; k < nkeys; ++k)
+      if (jb.top_of[k] > 0) top = k;
+  return top;
+}
 struct CompactJobs {
   CompactJob j[6 + 2 * kMaxPeers];
   int njobs;
@@ -1448,6 +1460,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(CompactJobs jo
   const CompactJob jb = jobs.j[q];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < nkeys) running[threadIdx.x] = jb.counts[(size_t)threadIdx.x * jb.ntiles + tile];
+  const int skip = skipped_key(jb, nkeys);
   const int base = tile * kTile;
   const unsigned lt = (1u << lane) - 1u;
   for (int r = 0; r < kTile; r += blockDim.x) {
@@ -1460,7 +1473,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter(CompactJobs jo
       if (lane == 0) wcount[warp][kk] = __popc(mask);
     }
     __syncthreads();
-    if (k >= 0) {
+    if (k >= 0 && k != skip) {
       int pos = running[k] + rank;
       for (int w = 0; w < warp; ++w) pos += wcount[w][k];
       jb.list[pos] = jb.base + i;
@@ -1489,6 +1502,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter_packed(Compact
   const CompactJob jb = jobs.j[q];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int first = tile * kTile + threadIdx.x * IPT;
+  const int skip = skipped_key(jb, nkeys);
   int key[IPT];
   unsigned long long mine = 0;
 #pragma unroll
@@ -1513,7 +1527,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_tile_scatter_packed(Compact
     if (k < 0) continue;
     const int pos = jb.counts[(size_t)k * jb.ntiles + tile] + (int)((pre >> (12 * k)) & 0xfff);
     pre += 1ull << (12 * k);
-    jb.list[pos] = jb.base + first + j;
+    if (k != skip) jb.list[pos] = jb.base + first + j;
   }
 }
 

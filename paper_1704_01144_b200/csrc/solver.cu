@@ -206,6 +206,8 @@ struct tafv_gpu {
   bool led_pending = false;
   bool iwin_alias = true;
   int8_t *tau = nullptr, *cad = nullptr, *raw = nullptr, *tmpa = nullptr, *tmpb = nullptr;
+  int skip_top_lists = 1;         // flag "skip_top_lists": do not write the top level's list entries
+  bool lists_skip_top = false;    // the last plan's lists lack their top-level segment
   uint8_t* sweep_tile = nullptr;  // [sweep][cell tile] marks of the Jacobi sweeps (k_level_sweep)
   int sweep_marks = 1;            // flag "sweep_marks": skip the tiles no level change can reach
   uint8_t* fflag = nullptr;
@@ -1359,20 +1361,23 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
   // K3 list (owned cells by level), K2 list (faces touching owned by cadence),
   // shards' K1 list: prefixes of each are the active sets of every level
   CompactJobs jobs{};
+  // single domain: the top level's entries are never read (identity phases)
+  h.lists_skip_top = !h.sharded() && h.skip_top_lists;
+  const long long* top_of = h.lists_skip_top ? &h.dplan->cell_count[0] : nullptr;
   jobs.j[0] = CompactJob{h.tau, h.n_own, ntc, h.cell_counts, h.clist, &h.dplan->cell_count[0],
-                         &h.dplan->ncell_prefix[0], 0};
+                         &h.dplan->ncell_prefix[0], 0, top_of};
   jobs.j[1] = CompactJob{h.cad, h.F_own, h.ntile_f, h.face_counts, h.flist, &h.dplan->face_count[0],
-                         &h.dplan->nface_prefix[0], 0};
+                         &h.dplan->nface_prefix[0], 0, top_of};
   jobs.njobs = 2;
   if (k1) {
     jobs.j[2] = CompactJob{h.tau, h.n_deep, std::max(1, h.ntile_k), h.k1_counts, h.klist,
-                           &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0], 0};
+                           &h.dplan->k1_count[0], &h.dplan->nk1_prefix[0], 0, nullptr};
     jobs.j[3] = CompactJob{h.tau + h.n_deep, h.n_k1 - h.n_deep, std::max(1, h.ntile_kb), h.kb_counts,
-                           h.kblist, &h.dplan->kb_count[0], &h.dplan->nkb_prefix[0], h.n_deep};
+                           h.kblist, &h.dplan->kb_count[0], &h.dplan->nkb_prefix[0], h.n_deep, nullptr};
     jobs.j[4] = CompactJob{h.cad, h.F_int, std::max(1, h.ntile_fi), h.fi_counts, h.filist,
-                           &h.dplan->fi_count[0], &h.dplan->nfi_prefix[0], 0};
+                           &h.dplan->fi_count[0], &h.dplan->nfi_prefix[0], 0, nullptr};
     jobs.j[5] = CompactJob{h.cad + h.F_int, h.F_own - h.F_int, std::max(1, h.ntile_fb), h.fb_counts, h.fblist,
-                           &h.dplan->fb_count[0], &h.dplan->nfb_prefix[0], h.F_int};
+                           &h.dplan->fb_count[0], &h.dplan->nfb_prefix[0], h.F_int, nullptr};
     jobs.njobs = 6;
   }
   if (h.xfilter) {  // the exchange lists of every peer, sorted by level
@@ -1392,7 +1397,8 @@ void enqueue_finish_plan(tafv_gpu& h, int nkeys, bool cells_counted) {
         ++h.launches;
         jobs.j[jobs.njobs++] = CompactJob{key, n, nt, cnt, (side ? h.xpos_r : h.xpos_s) + off,
                                           side ? &h.dplan->xr_count[q][0] : &h.dplan->xs_count[q][0],
-                                          side ? &h.dplan->xr_prefix[q][0] : &h.dplan->xs_prefix[q][0], off};
+                                          side ? &h.dplan->xr_prefix[q][0] : &h.dplan->xs_prefix[q][0], off,
+                                          nullptr};
       }
     }
   }
@@ -2268,9 +2274,20 @@ int tafv_gpu_get_plan_lists(tafv_gpu* h, int32_t* tau_out, int32_t* cad_out, int
     const int L = h->theta + 1;
     // Device lists (internal ids, level-sorted) -> original ids, ascending per level.
     auto export_list = [&](const int* dlist, long long n_total, const long long* counts,
-                           const std::vector<int>& perm, int32_t* out) {
+                           const std::vector<int>& perm, int32_t* out, const std::vector<int8_t>& key,
+                           long long n_items) {
       std::vector<int> lst(n_total);
       if (n_total) CK(cudaMemcpy(lst.data(), dlist, n_total * sizeof(int), cudaMemcpyDeviceToHost));
+      if (h->lists_skip_top) {
+        // the device list has no entries for the top level theta (never read
+        // there): the items with key == theta in ascending internal id, which
+        // is what the stable compaction would have written
+        long long o = 0;
+        for (int l = 0; l < h->theta; ++l) o += counts[l];
+        for (long long i = 0; i < n_items; ++i)
+          if (key[i] == h->theta) lst[o++] = (int)i;
+        if (o != n_total) throw std::logic_error("plan lists: top-level count mismatch");
+      }
       long long o = 0;
       for (int l = 0; l < L; ++l) {
         for (long long i = o; i < o + counts[l]; ++i) out[i] = perm[lst[i]];
@@ -2283,8 +2300,8 @@ int tafv_gpu_get_plan_lists(tafv_gpu* h, int32_t* tau_out, int32_t* cad_out, int
       nc += h->ccount[l];
       nf += h->fcount[l];
     }
-    if (cells_flat) export_list(h->clist, nc, h->ccount, h->cperm, cells_flat);
-    if (faces_flat) export_list(h->flist, nf, h->fcount, h->fperm, faces_flat);
+    if (cells_flat) export_list(h->clist, nc, h->ccount, h->cperm, cells_flat, tau, h->n_own);
+    if (faces_flat) export_list(h->flist, nf, h->fcount, h->fperm, faces_flat, cad, h->F_own);
     if (fringe_flat) {
       // fringe[l]: cells of level l+1 flagged by a level-l face neighbour
       // (levels.cpp:139-153), from the device flags.
@@ -2994,6 +3011,9 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
     h->twin = nullptr;
     if (n == "grid_cap") {
       h->grid_cap = (int)std::max<int64_t>(1, std::min<int64_t>(value, h->nblk_last));
+      drop_graphs(*h);
+    } else if (n == "skip_top_lists") {
+      h->skip_top_lists = value != 0;
       drop_graphs(*h);
     } else if (n == "sweep_marks") {
       h->sweep_marks = value != 0;

@@ -325,12 +325,15 @@ def test_graph_and_direct_launch_bitwise(use_graph, slot_geo, iwin_alias, gpu):
     assert [r["t_start"] for r in rg] == [r["t_start"] for r in ro]
 
 
+@pytest.mark.parametrize("flag", ["sweep_marks", "skip_top_lists"])
 @pytest.mark.parametrize("cid,scale,iters", [(3, 8, 5), (4, 10, 4), (2, 4, 6)])
-def test_sweep_tile_marks_are_invisible(cid, scale, iters, gpu):
-    """The Jacobi sweeps of plan_iteration with the per-tile change marks
-    (sweep i + 1 re-evaluates only the tiles a level change of sweep i can
-    reach, the rest is copied) leave bit-exact the level map, every plan list,
-    the records and the state of the sweeps without them (levels.cpp:33-51);
+def test_plan_shortcuts_are_invisible(cid, scale, iters, flag, gpu):
+    """Two exact shortcuts of plan_iteration, each against the plan without
+    it: the Jacobi sweeps with per-tile change marks (sweep i + 1 re-evaluates
+    only the tiles a level change of sweep i can reach, the rest is copied;
+    levels.cpp:33-51), and level-sorted lists whose top-level entries are not
+    written on the device (no phase reads them; get_plan_lists rebuilds them
+    from the level map). Bit-exact level map, plan lists, records and state;
     several tiles and levels that move between iterations."""
     cfg = configs.get(cid, scale)
     mesh = cfg.mesh()
@@ -339,7 +342,7 @@ def test_sweep_tile_marks_are_invisible(cid, scale, iters, gpu):
     runs = []
     for marks in (1, 0):
         g = Solver(mesh, "euler")
-        g.set_flag("sweep_marks", marks)
+        g.set_flag(flag, marks)
         g.set_state(w0)
         lists, recs = [], []
         for _ in range(iters):
