@@ -1101,9 +1101,6 @@ __global__ void __launch_bounds__(256) k_totals(const DD* partials, int nblocks,
 // them into plan->dt_min. With tau != null (synthetic level maps) the bound is
 // dt_max / 2^tau. `reset` (plan_iteration): that block also clears the plan's
 // error flag and counts for the counting kernels that follow.
-#ifndef TAFV_DT_ROW128
-#define TAFV_DT_ROW128 1
-#endif
 template <class P>
 __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParams pp, double cfl,
                                                 double dt_cap, double* dt_max, double* block_min,
@@ -1115,12 +1112,8 @@ __global__ void __launch_bounds__(256) k_dt_max(MeshDev m, StateDev s, PhysParam
   const int stride = gridDim.x * blockDim.x;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
     double w[NV];
-#if TAFV_DT_ROW128
-    load_row<NV, true>(s.w, c, w);
-#else
 #pragma unroll
     for (int k = 0; k < NV; ++k) w[k] = s.w[(size_t)c * NV + k];
-#endif
     const double speed = P::speed(pp, w);
     const double d = speed > 0.0 ? smin(dt_cap, cfl * m.chl[c] / speed) : dt_cap;
     dt_max[c] = d;
