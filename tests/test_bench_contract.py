@@ -36,7 +36,8 @@ def test_reference_arm_line_contract():
             "'--warmup', '0', '--sample-cells', '200000', '--no-scalar2d']; "
             "runpy.run_path('bench.py', run_name='__main__'); "
             "maps = [l.split()[-1] for l in open('/proc/self/maps') if l.rstrip().endswith('.so')]; "
-            "print(json.dumps({'maps': sorted(set(m for m in maps if '/root/repo' in m or 'repo' in m))}))")
+            "import os; root = os.path.realpath('.'); "
+            "print(json.dumps({'maps': sorted(set(m for m in maps if os.path.realpath(m).startswith(root)))}))")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [json.loads(l) for l in out.stdout.strip().splitlines() if l.startswith("{")]
