@@ -206,10 +206,25 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
  * "repartition_ms" [1] (double: wall time of the last repartition). */
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
 
-/* Launch configuration knobs (bench/profiling):
+/* Launch configuration knobs (bench/profiling; every setting leaves the
+ * results bitwise unchanged -- each has a parity test -- and drops the
+ * captured graphs):
  *   "grid_cap"       max blocks per grid-stride launch;
  *   "kernel_timing"  1: time every hot kernel with CUDA events on the
- *                    library stream (resets the per-kind totals). */
+ *                    library stream (resets the per-kind totals);
+ *   "use_graph", "plan_graph"  0: direct launches instead of the captured
+ *                    sweep / plan graphs;
+ *   "k1_tile"        identity-phase K1 with Morton-brick staging (-1 auto);
+ *   "k1_brick"       identity-phase K1 with bulk-copied brick streams (off);
+ *   "slot_geo", "slot_n", "slot_dx", "face_dx"  0: per-face geometry /
+ *                    centroid gathers instead of the per-slot / per-face
+ *                    offset streams;
+ *   "iwin_alias"     0: materialise int_window of equal-level faces;
+ *   "alt_dir"        0: every kernel walks its items forwards;
+ *   "sweep_marks"    0: every Jacobi sweep re-evaluates every tile;
+ *   "skip_top_lists" 0: write the top level's entries of the level-sorted
+ *                    lists too;
+ *   "batch_lanes", "dl_stream"  run_batch lanes / download stream. */
 int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value);
 
 /* Kernel launches issued by the last run/iterate/advance call (own kernels
