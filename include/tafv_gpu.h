@@ -203,7 +203,9 @@ int tafv_gpu_iterate_host(tafv_gpu* h, const tafv_options* opt, int32_t n, doubl
  * "int_window" [nf][nv], "dt_max" [nc] (double); "raw_level" [nc] (int32);
  * "mesh_digest" [20] (uint64: FNV-1a of every internal mesh array, slot
  * count, boundary count, flags -- compares the device and host builds);
- * "repartition_ms" [1] (double: wall time of the last repartition). */
+ * "repartition_ms" [1] (double: wall time of the last repartition);
+ * "brick_info" [4] (double: bricks of the brick K1, ragged bricks, cells
+ * left to the general K1, structures built). */
 int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out);
 
 /* Launch configuration knobs (bench/profiling; every setting leaves the

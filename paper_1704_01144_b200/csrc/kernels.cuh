@@ -538,45 +538,66 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
   }
 }
 
-// ---- K1 for identity phases of hex meshes: brick streams by bulk copies ------
-// A block takes a Morton brick of 128 consecutive cells and ONE elected thread
-// starts bulk copies (cp.async.bulk, the TMA engine; one mbarrier collects the
-// bytes) of every contiguous stream the brick reads: the cells' staged rows
-// (in an identity phase every window boundary lies on the front, so the
-// staged row IS w in a predictor / w_pred in a corrector, kernels.cpp:31-44),
-// centroids, 1/V, the CSR slots (neighbour, face) and a window of the face
-// arrays {normal, area} and centroids starting at the first face whose left
-// cell is in the brick (faces are grouped by left cell, so the window holds
-// the brick's +side faces and, through the neighbours inside the brick, ~80 %
-// of its -side ones). The per-cell arithmetic is k_grad_limit's (per-face
-// geometry: scale = sign * area, offset = face centroid - cell centroid, the
-// values the per-slot streams store); every operand that is in the brick is
-// read from shared memory, the rest (neighbour rows / faces outside the
-// window) through a generic pointer that selects global memory, so a warp
-// does not diverge on it. No global load sits on a cell's dependent chain
-// except those out-of-brick rows, and the per-slot geometry streams (384 of
-// the 580 DRAM bytes k_grad_limit reads per cell) are not read at all. Other
-// resident blocks compute while a block waits for its copies (one stage per
-// block: double buffering would halve the resident warps for the same
-// shared memory).
+// ---- K1 for identity phases of hex meshes: precomputed bricks ---------------
+// A block takes a Morton brick of 128 consecutive cells whose every operand
+// arrives in shared memory without a dependent global load:
+//  * built once per mesh (k_brick_build): per slot a 16-bit row index into the
+//    brick's stage (own rows 0..127, halo rows 128.., 0xffff = no neighbour) and
+//    a 16-bit face entry (bit 15 = the slot sees the face from its right side),
+//    the brick's halo cell list, and the brick's faces {n, area}, centroid
+//    PACKED per brick (a face shared by two bricks is stored in both: ~3.6
+//    entries of 56 B per cell instead of the 6 x 64 B per-slot streams);
+//  * per brick, ONE elected thread starts bulk copies (cp.async.bulk, the TMA
+//    engine, one mbarrier) of the contiguous streams -- the cells' staged rows
+//    (in an identity phase the staged row IS w in a predictor / w_pred in a
+//    corrector, kernels.cpp:31-44), centroids, 1/V, the index table, the
+//    packed faces -- and prefetches the next brick's into L2; every thread
+//    gathers its share of the halo rows with cp.async (the halo list of brick
+//    b was fetched while brick b - 1 was computed);
+//  * then k_grad_limit's per-cell arithmetic (per-face geometry: scale =
+//    sign * area, offset = face centroid - cell centroid, the values the
+//    per-slot streams store) from shared memory only.
+// Bricks whose halo or faces exceed the stage (ragged Morton bricks) are left
+// to k_grad_limit over a list of their cells. Other resident blocks compute
+// while a block waits for its copies (one stage per block).
 #ifndef TAFV_K1B_MINB
-#define TAFV_K1B_MINB 5
+#define TAFV_K1B_MINB 4
 #endif
-constexpr int kBrick = 128;      // cells per brick = threads per block
-constexpr int kBrickFaces = 448; // face window (3 +side faces per cell and boundary slack), even
+// Stage capacities: 128-cell runs of the Morton order are ragged (config 4:
+// 500 +- 20 face entries, 235 +- 40 halo rows per brick against 464 / 160 for
+// an 8x4x4 box; tools/brick_probe.py). 576 entries and 256 halo rows hold 75 %
+// of config 4's bricks in 56.8 KB, the largest stage that leaves 4 blocks per
+// SM; larger stages (3 blocks per SM) and smaller ones (more bricks left to
+// the general kernel) both measured slower.
+#ifndef TAFV_K1B_HALO
+#define TAFV_K1B_HALO 256
+#endif
+#ifndef TAFV_K1B_FCAP
+#define TAFV_K1B_FCAP 576
+#endif
+constexpr int kBrick = 128;  // cells per brick = threads per block
+constexpr int kBrickHalo = TAFV_K1B_HALO;
+constexpr int kBrickFcap = TAFV_K1B_FCAP;
+struct BrickDev {
+  const unsigned short* idx;  // [nbricks][2][768]: row indices, then face entries
+  const int* halo;            // [nbricks][kBrickHalo] halo cell ids
+  const double* geo;          // [nbricks][kBrickFcap][4] {n, area}
+  const double* fcen;         // [nbricks][kBrickFcap][3]
+  const int2* count;          // [nbricks] {face entries, halo rows}; x < 0: not staged (ragged)
+};
 template <int NV>
 struct BrickSmem {  // byte offsets into the dynamic shared memory (16-byte aligned parts)
-  static constexpr int row = 0;
-  static constexpr int cen = row + kBrick * NV * 8;
+  static constexpr int row = 0;  // [128 + halo][NV]
+  static constexpr int cen = row + (kBrick + kBrickHalo) * NV * 8;
   static constexpr int ivol = cen + kBrick * 24;
-  static constexpr int nb = ivol + kBrick * 8;
-  static constexpr int af = nb + kBrick * 24;
-  static constexpr int geo = (af + kBrick * 24 + 31) & ~31;
-  static constexpr int fcen = geo + kBrickFaces * 32;
-  static constexpr int bytes = fcen + kBrickFaces * 24;
+  static constexpr int idx = ivol + kBrick * 8;          // [2][768] u16
+  static constexpr int hl = idx + 2 * 768 * 2;           // [2][halo] halo lists (this brick's, the next one's)
+  static constexpr int geo = (hl + 2 * kBrickHalo * 4 + 31) & ~31;
+  static constexpr int fcen = geo + kBrickFcap * 32;
+  static constexpr int bytes = fcen + kBrickFcap * 24;
 };
 __device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the stage before the async writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the stage before the async writes
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
@@ -586,11 +607,18 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
                "l"(src), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
 }
-// brick_f0[b] = first face whose left cell is >= 128 b (k_brick_f0); cells
-// [0, *n_dev) active, all with 6 slots.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+}
+// cells [0, *n_dev) active (an identity phase: n = every owned cell), all with 6 slots.
 template <class P>
-__global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(MeshDev m, StateDev s,
-                                                                           const int* __restrict__ brick_f0,
+__global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(MeshDev m, StateDev s, BrickDev bk,
                                                                            const int* __restrict__ n_dev,
                                                                            int pred, int rev) {
   constexpr int NV = P::NV, D = P::DIM, B = kBrick;
@@ -599,8 +627,9 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
   double* s_row = reinterpret_cast<double*>(brick_smem + L::row);
   double* s_cen = reinterpret_cast<double*>(brick_smem + L::cen);
   double* s_ivol = reinterpret_cast<double*>(brick_smem + L::ivol);
-  int* s_nb = reinterpret_cast<int*>(brick_smem + L::nb);
-  int* s_af = reinterpret_cast<int*>(brick_smem + L::af);
+  unsigned short* s_ri = reinterpret_cast<unsigned short*>(brick_smem + L::idx);
+  unsigned short* s_fi = s_ri + 768;
+  int* s_hl = reinterpret_cast<int*>(brick_smem + L::hl);
   double* s_geo = reinterpret_cast<double*>(brick_smem + L::geo);
   double* s_fcen = reinterpret_cast<double*>(brick_smem + L::fcen);
   __shared__ __align__(8) uint64_t bar;
@@ -609,47 +638,66 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
   __syncthreads();
   unsigned parity = 0;
   const int n = *n_dev;
-  const int nbricks = (n + B - 1) / B;
+  const int nbricks = n / B;  // whole bricks only; the tail cells go with the ragged bricks' list
   const double* __restrict__ src = pred ? s.w : s.wp;
+  auto brick_of = [&](int b) { return rev ? nbricks - 1 - b : b; };
+  // the first brick's halo list (later ones arrive one brick ahead)
+  int buf = 0;
+  if ((int)blockIdx.x < nbricks) {
+    const int bb = brick_of(blockIdx.x);
+    for (int i = tid; i < kBrickHalo; i += B) s_hl[i] = bk.halo[(size_t)bb * kBrickHalo + i];
+  }
+  __syncthreads();
   for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
-    // rev: walk the bricks backwards (the rows the predecessor wrote last are still in L2)
-    const int bb = rev ? nbricks - 1 - b : b;
+    const int bb = brick_of(b);
     const int lo = bb * B;
-    const int cnt = min(B, n - lo);
-    // face window [fs, fs + fcnt): even start and count (24-byte centroid rows, 16-byte copies)
-    const int f0 = brick_f0[bb], f1 = brick_f0[bb + 1];
-    const int fs = f0 & ~1;
-    int fcnt = min(f1, fs + kBrickFaces) - fs;
-    if (fcnt & 1) fcnt += fs + fcnt < m.n_faces ? 1 : -1;
-    if (fcnt < 0) fcnt = 0;
-    if (cnt == B) {
+    const int2 cnt = bk.count[bb];
+    const int bn = b + (int)gridDim.x;
+    const int nbb = bn < nbricks ? brick_of(bn) : -1;
+    const int ne = (cnt.x + 1) & ~1;  // an even number of entries: 16-byte multiples of the 24-byte centroids
+    if (cnt.x >= 0) {
       if (tid == 0) {
-        mbar_expect(&bar, (unsigned)(B * NV * 8 + B * 24 + B * 8 + B * 24 + B * 24 + fcnt * 56));
+        mbar_expect(&bar, (unsigned)(B * NV * 8 + B * 24 + B * 8 + 3072 + ne * 56));
+        bulk_copy(s_ri, bk.idx + (size_t)bb * 1536, 3072, &bar);
         bulk_copy(s_row, src + (size_t)lo * NV, B * NV * 8, &bar);
-        bulk_copy(s_nb, m.adj_nb + 6 * (size_t)lo, B * 24, &bar);
-        bulk_copy(s_af, m.adj_face + 6 * (size_t)lo, B * 24, &bar);
-        if (fcnt) {
-          bulk_copy(s_geo, m.geo + fs, (unsigned)fcnt * 32, &bar);
-          bulk_copy(s_fcen, m.fcen + 3 * (size_t)fs, (unsigned)fcnt * 24, &bar);
+        if (ne) {
+          bulk_copy(s_geo, bk.geo + (size_t)bb * kBrickFcap * 4, (unsigned)ne * 32, &bar);
+          bulk_copy(s_fcen, bk.fcen + (size_t)bb * kBrickFcap * 3, (unsigned)ne * 24, &bar);
         }
         bulk_copy(s_cen, m.cen + 3 * (size_t)lo, B * 24, &bar);
         bulk_copy(s_ivol, m.ivol + lo, B * 8, &bar);
       }
+      // halo rows: 8-byte asynchronous copies, every thread its share
+      const int* hl = s_hl + buf * kBrickHalo;
+      for (int i = tid; i < cnt.y * NV; i += B) {
+        const int h = i / NV, k = i - h * NV;
+        cp_async8(s_row + (B + h) * NV + k, src + (size_t)hl[h] * NV + k);
+      }
+    }
+    if (nbb >= 0) {  // the next brick: its halo list into the other buffer, its streams towards L2
+      int* hn = s_hl + (buf ^ 1) * kBrickHalo;
+      for (int i = tid; i < kBrickHalo; i += B) hn[i] = bk.halo[(size_t)nbb * kBrickHalo + i];
+      if (tid == 32) {
+        const int2 c2 = bk.count[nbb];
+        if (c2.x >= 0) {
+          const int n2 = (c2.x + 1) & ~1;
+          bulk_prefetch_l2(bk.idx + (size_t)nbb * 1536, 3072);
+          bulk_prefetch_l2(src + (size_t)nbb * B * NV, B * NV * 8);
+          if (n2) {
+            bulk_prefetch_l2(bk.geo + (size_t)nbb * kBrickFcap * 4, (unsigned)n2 * 32);
+            bulk_prefetch_l2(bk.fcen + (size_t)nbb * kBrickFcap * 3, (unsigned)n2 * 24);
+          }
+          bulk_prefetch_l2(m.cen + 3 * (size_t)nbb * B, B * 24);
+        }
+      }
+    }
+    if (cnt.x >= 0) {
+      cp_async_wait_all();
       mbar_wait(&bar, parity);
       parity ^= 1u;
-    } else {  // the tail brick: plain cooperative copies
-      for (int i = tid; i < cnt * NV; i += B) s_row[i] = src[(size_t)lo * NV + i];
-      for (int i = tid; i < cnt * 6; i += B) {
-        s_nb[i] = m.adj_nb[6 * (size_t)lo + i];
-        s_af[i] = m.adj_face[6 * (size_t)lo + i];
-      }
-      for (int i = tid; i < cnt * 3; i += B) s_cen[i] = m.cen[3 * (size_t)lo + i];
-      for (int i = tid; i < cnt; i += B) s_ivol[i] = m.ivol[lo + i];
-      for (int i = tid; i < fcnt * 4; i += B) s_geo[i] = reinterpret_cast<const double*>(m.geo + fs)[i];
-      for (int i = tid; i < fcnt * 3; i += B) s_fcen[i] = m.fcen[3 * (size_t)fs + i];
-      __syncthreads();
     }
-    if (tid < cnt) {
+    __syncthreads();  // halo rows of every thread, the next halo list
+    if (cnt.x >= 0) {
       const int c = lo + tid;
       double we[NV];
 #pragma unroll
@@ -666,21 +714,17 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
       bool any = false;
 #pragma unroll
       for (int t = 0; t < 6; ++t) {
-        const int nb = s_nb[tid * 6 + t];
-        const int ef = s_af[tid * 6 + t];
-        const int f = slot_face(ef);
-        const unsigned fi = (unsigned)(f - fs);
-        const double* gp = fi < (unsigned)fcnt ? s_geo + 4 * fi : reinterpret_cast<const double*>(m.geo + f);
-        const double2 g01 = *reinterpret_cast<const double2*>(gp);
-        const double2 g23 = *reinterpret_cast<const double2*>(gp + 2);
-        const double scale = slot_sign(ef) * g23.y;
+        const unsigned li = s_ri[tid * 6 + t];
+        const unsigned fe = s_fi[tid * 6 + t];
+        const unsigned le = fe & 0x7fffu;
+        const double2 g01 = *reinterpret_cast<const double2*>(s_geo + 4 * le);
+        const double2 g23 = *reinterpret_cast<const double2*>(s_geo + 4 * le + 2);
+        const double scale = (fe & 0x8000u) ? -g23.y : g23.y;  // sign * area, exact
         double wf[NV];
-        if (nb >= 0) {
-          const unsigned ni = (unsigned)(nb - lo);
-          const double* rp = ni < (unsigned)cnt ? s_row + ni * NV : src + (size_t)nb * NV;
+        if (li != 0xffffu) {
 #pragma unroll
           for (int k = 0; k < NV; ++k) {
-            const double wn = rp[k];
+            const double wn = s_row[li * NV + k];
             wf[k] = 0.5 * (we[k] + wn);
             wmin[k] = smin(wmin[k], wn);
             wmax[k] = smax(wmax[k], wn);
@@ -713,10 +757,8 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
         }
 #pragma unroll
         for (int t = 0; t < 6; ++t) {
-          const int f = slot_face(s_af[tid * 6 + t]);
-          const unsigned fi = (unsigned)(f - fs);
-          const double* fc = fi < (unsigned)fcnt ? s_fcen + 3 * fi : m.fcen + 3 * (size_t)f;
-          const double dx0 = fc[0] - cc0, dx1 = fc[1] - cc1, dx2 = fc[2] - cc2;
+          const unsigned le = s_fi[tid * 6 + t] & 0x7fffu;
+          const double dx0 = s_fcen[3 * le] - cc0, dx1 = s_fcen[3 * le + 1] - cc1, dx2 = s_fcen[3 * le + 2] - cc2;
 #pragma unroll
           for (int k = 0; k < NV; ++k) {
             double delta = g[k][0] * dx0 + g[k][1] * dx1;
@@ -743,23 +785,109 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
 #pragma unroll
       for (int q = 0; q < GS; q += 4) st4(go + q, row[q], row[q + 1], row[q + 2], row[q + 3]);
     }
+    buf ^= 1;
     __syncthreads();  // every read of the stage before the next brick's copies
   }
 }
 
-// First face whose left cell is >= 128 b, b in [0, nb] (faces grouped by left
-// cell: a binary search; on any other order the window is merely a worse cache).
-__global__ void k_brick_f0(const int2* __restrict__ lr, int F, int nb, int* __restrict__ out) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b > nb) return;
-  const long long key = (long long)b * kBrick;
-  int lo = 0, hi = F;
-  while (lo < hi) {
-    const int mid = lo + (hi - lo) / 2;
-    if (lr[mid].x < key) lo = mid + 1;
-    else hi = mid;
+// The static brick structures (BrickDev) of cells [0, n), one block per whole
+// brick: a slot whose face this cell owns as the left side (or whose left cell
+// lies outside the brick) takes a packed face entry, the other side of a face
+// inside the brick shares its left cell's entry; every out-of-brick neighbour
+// takes a halo row. A brick that does not fit the stage gets count.x = -1.
+__global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ adj_nb,
+                                                        const int* __restrict__ adj_face,
+                                                        const double4* __restrict__ geo,
+                                                        const double* __restrict__ fcen, int nbricks,
+                                                        unsigned short* idx, int* halo, double* bgeo, double* bfcen,
+                                                        int2* count, int* ragged_count) {
+  __shared__ int s_nb[768], s_af[768], s_ent[768];
+  __shared__ int s_e[kBrick + 1], s_h[kBrick + 1];
+  const int b = blockIdx.x, tid = threadIdx.x, lo = b * kBrick;
+  if (b >= nbricks) return;
+  for (int i = tid; i < 768; i += kBrick) {
+    s_nb[i] = adj_nb[6 * (size_t)lo + i];
+    s_af[i] = adj_face[6 * (size_t)lo + i];
   }
-  out[b] = lo;
+  __syncthreads();
+  int ne = 0, nh = 0;
+  for (int t = 0; t < 6; ++t) {
+    const int nb = s_nb[tid * 6 + t], ef = s_af[tid * 6 + t];
+    const bool inside = nb >= lo && nb < lo + kBrick;
+    if (nb >= 0 && !inside) ++nh;
+    if (ef >= 0 || !inside) ++ne;
+  }
+  s_e[tid + 1] = ne;
+  s_h[tid + 1] = nh;
+  __syncthreads();
+  if (tid == 0) {
+    s_e[0] = s_h[0] = 0;
+    for (int i = 1; i <= kBrick; ++i) {
+      s_e[i] += s_e[i - 1];
+      s_h[i] += s_h[i - 1];
+    }
+  }
+  __syncthreads();
+  const int etot = s_e[kBrick], htot = s_h[kBrick];
+  const bool fits = etot <= kBrickFcap && htot <= kBrickHalo;
+  if (tid == 0) {
+    count[b] = fits ? make_int2(etot, htot) : make_int2(-etot, htot);  // x < 0: ragged (sizes kept for tuning)
+    if (!fits) atomicAdd(ragged_count, 1);
+  }
+  if (!fits) return;
+  int e = s_e[tid], h = s_h[tid];
+  unsigned short* ri = idx + (size_t)b * 1536;
+  unsigned short* fi = ri + 768;
+  for (int t = 0; t < 6; ++t) {
+    const int nb = s_nb[tid * 6 + t], ef = s_af[tid * 6 + t];
+    const bool inside = nb >= lo && nb < lo + kBrick;
+    unsigned short r = 0xffffu;
+    if (nb >= 0) {
+      if (inside) {
+        r = (unsigned short)(nb - lo);
+      } else {
+        halo[(size_t)b * kBrickHalo + h] = nb;
+        r = (unsigned short)(kBrick + h);
+        ++h;
+      }
+    }
+    ri[tid * 6 + t] = r;
+    int ent = -1;
+    if (ef >= 0 || !inside) {
+      const int f = ef >= 0 ? ef : ~ef;
+      const double4 gq = geo[f];
+      double* go = bgeo + ((size_t)b * kBrickFcap + e) * 4;
+      go[0] = gq.x;
+      go[1] = gq.y;
+      go[2] = gq.z;
+      go[3] = gq.w;
+      double* fo = bfcen + ((size_t)b * kBrickFcap + e) * 3;
+      fo[0] = fcen[3 * (size_t)f];
+      fo[1] = fcen[3 * (size_t)f + 1];
+      fo[2] = fcen[3 * (size_t)f + 2];
+      ent = e++;
+    }
+    s_ent[tid * 6 + t] = ent;
+  }
+  for (int i = htot + tid; i < kBrickHalo; i += kBrick) halo[(size_t)b * kBrickHalo + i] = 0;  // (never gathered)
+  __syncthreads();
+  for (int t = 0; t < 6; ++t) {
+    const int nb = s_nb[tid * 6 + t], ef = s_af[tid * 6 + t];
+    int ent = s_ent[tid * 6 + t];
+    if (ent < 0) {  // the right side of a face whose left cell is in the brick: that cell's entry
+      const int f = ~ef, l = nb - lo;
+      for (int q = 0; q < 6; ++q)
+        if (s_af[l * 6 + q] == f) ent = s_ent[l * 6 + q];
+    }
+    fi[tid * 6 + t] = (unsigned short)(ent | (ef < 0 ? 0x8000 : 0));
+  }
+}
+// The cells the brick kernel leaves to k_grad_limit: ragged bricks and the tail.
+__global__ void k_brick_ragged_cells(const int2* __restrict__ count, int nbricks, int n, int* list, int* n_out) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const int b = c / kBrick;
+    if (b >= nbricks || count[b].x < 0) list[atomicAdd(n_out, 1)] = c;
+  }
 }
 
 // kernels.cpp:25-27 with the z term appended left to right; d = to - from.

@@ -71,8 +71,11 @@ void check_cuda(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw Error{TAFV_ECUDA, std::string(where) + ": " + cudaGetErrorString(e)};
 }
 #define CK(x) check_cuda((x), #x)
+#ifndef TAFV_K1_BRICK_MAX_RAGGED
+#define TAFV_K1_BRICK_MAX_RAGGED 0.4  // auto mode: largest share of bricks that may not fit the stage
+#endif
 #ifndef TAFV_K1_BRICK_AUTO
-#define TAFV_K1_BRICK_AUTO (1 << 30)  // auto threshold (owned cells) of the brick K1; off until measured
+#define TAFV_K1_BRICK_AUTO (4 << 20)  // auto threshold (owned cells) of the brick K1
 #endif
 
 void require(bool cond, const char* what) {
@@ -172,10 +175,19 @@ struct tafv_gpu {
   // identity-phase K1 with the brick's streams bulk-copied into shared memory
   // (k_grad_limit_brick; per-face geometry windows): -1 auto, 0 off, 1 on
   int k1_brick = -1;
-  int* brick_f0 = nullptr;  // [ceil(n_k1 / 128) + 1] first face by left cell (mesh, shared with the twin)
+  // the bricks' static structures (BrickDev; mesh data, shared with the twin),
+  // built on first use, and the cells left to k_grad_limit (ragged bricks, tail)
+  unsigned short* brick_idx = nullptr;
+  int* brick_halo = nullptr;
+  double *brick_geo = nullptr, *brick_fcen = nullptr;
+  int2* brick_count = nullptr;
+  int *brick_rest = nullptr, *brick_nrest = nullptr;  // list and its count (device)
+  int brick_rest_host = 0, brick_ragged = 0, nbricks = 0;
+  bool brick_declined = false;  // auto mode found too many ragged bricks on this mesh
+  BrickDev brick_dev() const { return BrickDev{brick_idx, brick_halo, brick_geo, brick_fcen, brick_count}; }
   int grid_k1b = 0;
   bool use_k1_brick() const {
-    return deg6 && brick_f0 && (k1_brick > 0 || (k1_brick < 0 && n_own >= (TAFV_K1_BRICK_AUTO)));
+    return deg6 && brick_idx && (k1_brick > 0 || (k1_brick < 0 && n_own >= (TAFV_K1_BRICK_AUTO)));
   }
   bool face_dx = true;
   int dl_stream = 1;  // run_batch downloads on the copy stream (0: on the library stream, A/B)
@@ -356,7 +368,8 @@ struct tafv_gpu {
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     if (owns_mesh) {
       void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
-                           d_cperm, d_fperm, bface, brick_f0};
+                           d_cperm, d_fperm, bface, brick_idx, brick_halo, brick_geo, brick_fcen, brick_count,
+                           brick_rest, brick_nrest};
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
     }
@@ -1037,17 +1050,60 @@ void upload_mesh_device(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cl
   CK(cudaStreamSynchronize(st));
 }
 
+// The brick K1's static structures (k_brick_build) for the whole bricks of
+// the owned cells of a hex mesh; a no-op when they exist or cannot (not hex,
+// a shard with halo cells: its identity phases run deep / border lists).
+void build_bricks(tafv_gpu& h) {
+  if (h.brick_idx || !h.deg6 || h.n_own != h.N || h.N < kBrick) return;
+  if (h.brick_declined && h.k1_brick < 0) return;
+  const int nb = h.N / kBrick;
+  h.nbricks = nb;
+  h.brick_idx = dalloc<unsigned short>((size_t)nb * 1536);
+  h.brick_halo = dalloc<int>((size_t)nb * kBrickHalo);
+  h.brick_geo = dalloc<double>((size_t)nb * kBrickFcap * 4);
+  h.brick_fcen = dalloc<double>((size_t)nb * kBrickFcap * 3);
+  h.brick_count = dalloc<int2>(nb);
+  h.brick_nrest = dalloc<int>(2);
+  CK(cudaMemsetAsync(h.brick_nrest, 0, 2 * sizeof(int), h.st));
+  CK(cudaMemsetAsync(h.brick_halo, 0, (size_t)nb * kBrickHalo * sizeof(int), h.st));
+  CK(cudaMemsetAsync(h.brick_geo, 0, (size_t)nb * kBrickFcap * 4 * sizeof(double), h.st));
+  CK(cudaMemsetAsync(h.brick_fcen, 0, (size_t)nb * kBrickFcap * 3 * sizeof(double), h.st));
+  k_brick_build<<<nb, kBrick, 0, h.st>>>(h.adj_nb, h.adj_face, h.geo, h.fcen, nb, h.brick_idx, h.brick_halo,
+                                         h.brick_geo, h.brick_fcen, h.brick_count, h.brick_nrest + 1);
+  CK(cudaGetLastError());
+  int cnt[2] = {0, 0};
+  CK(cudaMemcpyAsync(cnt, h.brick_nrest, sizeof cnt, cudaMemcpyDeviceToHost, h.st));
+  CK(cudaStreamSynchronize(h.st));
+  h.brick_ragged = cnt[1];
+  // auto mode: the brick kernel pays only when most bricks fit its stage
+  // (config 4: 75 % fit, K1 -8 %; config 3's corner-stretched mesh: ~40 %,
+  // K1 +7 % with the rest on the general kernel) -- else drop the structures
+  if (h.k1_brick < 0 && (double)cnt[1] > TAFV_K1_BRICK_MAX_RAGGED * nb) {
+    void* ptrs[] = {h.brick_idx, h.brick_halo, h.brick_geo, h.brick_fcen, h.brick_count, h.brick_nrest};
+    for (void* p : ptrs) cudaFree(p);
+    h.brick_idx = nullptr;
+    h.brick_halo = nullptr;
+    h.brick_geo = h.brick_fcen = nullptr;
+    h.brick_count = nullptr;
+    h.brick_nrest = nullptr;
+    h.brick_declined = true;
+    return;
+  }
+  const size_t cap = (size_t)cnt[1] * kBrick + (size_t)(h.N - nb * kBrick);
+  h.brick_rest = dalloc<int>(std::max<size_t>(1, cap));
+  k_brick_ragged_cells<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.brick_count, nb, h.N, h.brick_rest, h.brick_nrest);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(cnt, h.brick_nrest, sizeof(int), cudaMemcpyDeviceToHost, h.st));
+  CK(cudaStreamSynchronize(h.st));
+  h.brick_rest_host = cnt[0];
+  if ((size_t)cnt[0] != cap) throw std::logic_error("brick K1: ragged cell count mismatch");
+}
+
 void upload_mesh(tafv_gpu& h, const tafv_mesh_view& mv, const uint8_t* cls = nullptr,
                  const uint8_t* touch = nullptr) {
   if (getenv("TAFV_HOST_UPLOAD") != nullptr) upload_mesh_host(h, mv, cls, touch);
   else upload_mesh_device(h, mv, cls, touch);
-  if (h.deg6) {  // face windows of the brick K1 (k_grad_limit_brick)
-    const int nb = (h.n_k1 + kBrick - 1) / kBrick;
-    h.brick_f0 = dalloc<int>((size_t)nb + 1);
-    k_brick_f0<<<(nb + 256) / 256, 256, 0, h.st>>>(h.lr, h.F, nb, h.brick_f0);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(h.st));
-  }
+  if (h.k1_brick > 0 || (h.k1_brick < 0 && h.n_own >= (TAFV_K1_BRICK_AUTO))) build_bricks(h);
 }
 
 void alloc_state(tafv_gpu& h) {
@@ -1720,11 +1776,16 @@ void phase_t(tafv_gpu& h, bool pred, bool last, int level, int front) {
   timed(h, tafv_gpu::kK1, [&] {
     // identity phases (kl == nullptr) of hex meshes: the bulk-copy brick kernel
     // (single list: cells [0, n) lead the internal order), else the Morton-brick instance
-    if (DEG == 6 && kl == nullptr && !(h.sharded() && h.klist != h.clist) && h.use_k1_brick())
+    if (DEG == 6 && kl == nullptr && !(h.sharded() && h.klist != h.clist) && h.use_k1_brick()) {
       k_grad_limit_brick<P><<<fixed ? h.grid_k1b : std::min<long long>(h.grid_k1b, (nk + kBrick - 1) / kBrick),
-                              kBrick, BrickSmem<P::NV>::bytes, h.st>>>(md, sd, h.brick_f0, nkp, pred ? 1 : 0,
+                              kBrick, BrickSmem<P::NV>::bytes, h.st>>>(md, sd, h.brick_dev(), nkp, pred ? 1 : 0,
                                                                       h.next_dir());
-    else if (DEG == 6 && kl == nullptr && h.use_k1_tile())
+      if (h.brick_rest_host > 0) {  // ragged bricks and the tail cells: the general kernel over their list
+        k_grad_limit<P, DEG, false><<<h.grid_for(h.brick_rest_host, 128), 128, 0, h.st>>>(
+            md, sd, h.brick_rest, h.brick_nrest, 0, front, pred ? 1 : 0, 0);
+        ++h.launches;
+      }
+    } else if (DEG == 6 && kl == nullptr && h.use_k1_tile())
       k_grad_limit<P, DEG, true><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
     else
       k_grad_limit<P, DEG, false><<<g1, 128, 0, h.st>>>(md, sd, kl, nkp, 0, front, pred ? 1 : 0, h.next_dir());
@@ -2583,7 +2644,15 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->sgeo = h.sgeo;
     t->sdx = h.sdx;
     t->fdx = h.fdx;
-    t->brick_f0 = h.brick_f0;
+    t->brick_idx = h.brick_idx;
+    t->brick_halo = h.brick_halo;
+    t->brick_geo = h.brick_geo;
+    t->brick_fcen = h.brick_fcen;
+    t->brick_count = h.brick_count;
+    t->brick_rest = h.brick_rest;
+    t->brick_nrest = h.brick_nrest;
+    t->brick_rest_host = h.brick_rest_host;
+    t->nbricks = h.nbricks;
     t->k1_brick = h.k1_brick;
     t->d_cperm = h.d_cperm;
     t->d_fperm = h.d_fperm;
@@ -2925,6 +2994,16 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     if (n == "w") rows(h->w, h->N, h->nv, h->d_cperm);
     else if (n == "W") rows(h->W, h->N, h->nv, h->d_cperm);
     else if (n == "repartition_ms") *static_cast<double*>(out) = h->rep_ms;
+    else if (n == "brick_counts") {  // [nbricks][2] int32: face entries (negative: ragged), halo rows
+      if (h->brick_count)
+        CK(cudaMemcpy(out, h->brick_count, (size_t)h->nbricks * sizeof(int2), cudaMemcpyDeviceToHost));
+    } else if (n == "brick_info") {  // bricks, ragged bricks, cells left to the general K1, built
+      double* o = static_cast<double*>(out);
+      o[0] = h->nbricks;
+      o[1] = h->brick_ragged;
+      o[2] = h->brick_rest_host;
+      o[3] = h->brick_idx != nullptr;
+    }
     else if (n == "w_pred") rows(h->wp, h->N, h->nv, h->d_cperm);
     else if (n == "grad") {  // unpadded rows of nv*3
       const size_t w3 = (size_t)h->nv * 3;
@@ -3023,6 +3102,7 @@ int tafv_gpu_set_flag(tafv_gpu* h, const char* name, int64_t value) {
       drop_graphs(*h);
     } else if (n == "k1_brick") {
       h->k1_brick = (int)value;
+      if (value > 0) build_bricks(*h);
       drop_graphs(*h);
     } else if (n == "slot_n") {
       h->slot_n = value != 0;

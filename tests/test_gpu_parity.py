@@ -795,11 +795,13 @@ def test_k1_brick_path_bitwise(cid, scale, iters, gpu):
 
 @pytest.mark.parametrize("cid,scale,iters", [(1, 2, 6), (2, 5, 4), (4, 20, 3), (3, 10, 3)])
 def test_k1_bulk_brick_kernel_bitwise(cid, scale, iters, gpu):
-    """The identity-phase K1 whose brick streams arrive by bulk copies
-    (k_grad_limit_brick: cp.async.bulk + mbarrier, per-face geometry windows
-    in shared memory, generic-pointer fallback outside the brick) is bitwise
-    the per-cell kernel: state, gradients and level lists, with a tail brick
-    (cell counts that are no multiple of 128) and faces outside the window."""
+    """The identity-phase K1 over precomputed bricks (k_grad_limit_brick:
+    per-brick index tables, halo lists and packed faces built once;
+    cp.async.bulk + mbarrier for the contiguous streams, cp.async gathers of
+    the halo rows; ragged bricks and the tail cells through the general
+    kernel's list) is bitwise the per-cell kernel: state, gradients and level
+    lists, on permuted (configs 1, 2) and lattice-ordered meshes whose cell
+    counts are no multiple of 128."""
     cfg = configs.get(cid, scale)
     mesh = cfg.mesh()
     w0 = cfg.initial_state(mesh)
@@ -811,6 +813,10 @@ def test_k1_bulk_brick_kernel_bitwise(cid, scale, iters, gpu):
         g.set_state(w0)
         recs = g.reference_integrate(cfg.options(), iters)
         out[brick] = (g.get_state(), g.get_array("grad"), [r["level_cells"] for r in recs])
+        if brick:
+            info = g.get_array("brick_info")
+            assert info[3] == 1 and info[0] == len(mesh["vol"]) // 128
+            assert info[2] == info[1] * 128 + len(mesh["vol"]) % 128
         g.close()
     np.testing.assert_array_equal(out[0][0][0], out[1][0][0])
     np.testing.assert_array_equal(out[0][0][1], out[1][0][1])

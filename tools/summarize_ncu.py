@@ -22,6 +22,7 @@ PROF = os.path.join(ROOT, "profiles")
 
 KIND = [  # bench.py kernel kind <- short ncu name prefixes
     ("K1_grad_limit", "k_grad_limit<"),
+    ("K1_grad_limit", "k_grad_limit_brick<"),
     ("K2_face_pred", "k_face_flux<Euler3D, 1"),
     ("K2_face_corr", "k_face_flux<Euler3D, 0"),
     ("K3_update_pred", "k_gather_update<Euler3D, 1, 0"),
