@@ -295,7 +295,7 @@ class Solver:
         elif name == "brick_info":
             out = np.zeros(4)
         elif name == "brick_counts":
-            out = np.zeros((int(self.get_array("brick_info")[0]), 2), dtype=np.int32)
+            out = np.zeros((int(self.get_array("brick_info")[0]), 4), dtype=np.int32)
         else:
             rows = self.nf if name in ("phi_pred", "int_substep", "int_window") else self.nc
             width = {"grad": self.nv * 3, "dt_max": 1}.get(name, self.nv)

@@ -563,38 +563,42 @@ __global__ void __launch_bounds__(128, TAFV_K1_MINB) k_grad_limit(MeshDev m, Sta
 #ifndef TAFV_K1B_MINB
 #define TAFV_K1B_MINB 4
 #endif
-// Stage capacities: 128-cell runs of the Morton order are ragged (config 4:
+// Stage capacity: 128-cell runs of the Morton order are ragged (config 4:
 // 500 +- 20 face entries, 235 +- 40 halo rows per brick against 464 / 160 for
-// an 8x4x4 box; tools/brick_probe.py). 576 entries and 256 halo rows hold 75 %
-// of config 4's bricks in 56.8 KB, the largest stage that leaves 4 blocks per
-// SM; larger stages (3 blocks per SM) and smaller ones (more bricks left to
-// the general kernel) both measured slower.
+// an 8x4x4 box; tools/brick_probe.py), so the halo rows and the packed faces
+// share ONE pool of the stage -- a brick fits when 40 B per halo row + 56 B
+// per face entry fit the pool (and the halo list its buffer) -- sized for 4
+// blocks per SM; larger stages (3 blocks per SM) measured slower.
 #ifndef TAFV_K1B_HALO
-#define TAFV_K1B_HALO 256
+#define TAFV_K1B_HALO 320  // halo rows per brick at most (list buffers)
 #endif
-#ifndef TAFV_K1B_FCAP
-#define TAFV_K1B_FCAP 576
+#ifndef TAFV_K1B_POOL
+#define TAFV_K1B_POOL 41856  // bytes of halo rows + face entries per brick
 #endif
 constexpr int kBrick = 128;  // cells per brick = threads per block
 constexpr int kBrickHalo = TAFV_K1B_HALO;
-constexpr int kBrickFcap = TAFV_K1B_FCAP;
+constexpr int kBrickPool = TAFV_K1B_POOL;
+// pool bytes of a brick with e face entries (padded to even) and h halo rows of nv doubles
+__host__ __device__ constexpr int brick_pool_bytes(int e, int h, int nv) {
+  return ((h * nv * 8 + 31) & ~31) + ((e + 1) & ~1) * 56;
+}
 struct BrickDev {
   const unsigned short* idx;  // [nbricks][2][768]: row indices, then face entries
-  const int* halo;            // [nbricks][kBrickHalo] halo cell ids
-  const double* geo;          // [nbricks][kBrickFcap][4] {n, area}
-  const double* fcen;         // [nbricks][kBrickFcap][3]
-  const int2* count;          // [nbricks] {face entries, halo rows}; x < 0: not staged (ragged)
+  const int4* info;           // [nbricks] {face entries (< 0: ragged, not staged), halo rows, entry offset, halo offset}
+  const int* halo;            // halo cell ids, brick after brick (each padded to 4)
+  const double* geo;          // [entries][4] {n, area}, brick after brick (each padded to even)
+  const double* fcen;         // [entries][3]
 };
 template <int NV>
 struct BrickSmem {  // byte offsets into the dynamic shared memory (16-byte aligned parts)
-  static constexpr int row = 0;  // [128 + halo][NV]
-  static constexpr int cen = row + (kBrick + kBrickHalo) * NV * 8;
+  static constexpr int row = 0;  // [128][NV] own rows, then the pool: halo rows, {n, area}, centroids
+  static constexpr int pool = row + kBrick * NV * 8;
+  static constexpr int cen = pool + kBrickPool;
   static constexpr int ivol = cen + kBrick * 24;
-  static constexpr int idx = ivol + kBrick * 8;          // [2][768] u16
-  static constexpr int hl = idx + 2 * 768 * 2;           // [2][halo] halo lists (this brick's, the next one's)
-  static constexpr int geo = (hl + 2 * kBrickHalo * 4 + 31) & ~31;
-  static constexpr int fcen = geo + kBrickFcap * 32;
-  static constexpr int bytes = fcen + kBrickFcap * 24;
+  static constexpr int idx = ivol + kBrick * 8;  // [2][768] u16
+  static constexpr int hl = idx + 2 * 768 * 2;   // [2][halo] halo lists (this brick's, the next one's)
+  static constexpr int bytes = hl + 2 * kBrickHalo * 4;
+  static_assert(pool % 32 == 0 && kBrickPool % 32 == 0, "the pool holds 32-byte aligned face rows");
 };
 __device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses of the stage before the async writes
@@ -630,8 +634,6 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
   unsigned short* s_ri = reinterpret_cast<unsigned short*>(brick_smem + L::idx);
   unsigned short* s_fi = s_ri + 768;
   int* s_hl = reinterpret_cast<int*>(brick_smem + L::hl);
-  double* s_geo = reinterpret_cast<double*>(brick_smem + L::geo);
-  double* s_fcen = reinterpret_cast<double*>(brick_smem + L::fcen);
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   if (tid == 0) mbar_init(&bar, 1);
@@ -644,25 +646,29 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
   // the first brick's halo list (later ones arrive one brick ahead)
   int buf = 0;
   if ((int)blockIdx.x < nbricks) {
-    const int bb = brick_of(blockIdx.x);
-    for (int i = tid; i < kBrickHalo; i += B) s_hl[i] = bk.halo[(size_t)bb * kBrickHalo + i];
+    const int4 c0 = bk.info[brick_of(blockIdx.x)];
+    if (c0.x >= 0)
+      for (int i = tid; i < c0.y; i += B) s_hl[i] = bk.halo[(size_t)c0.w + i];
   }
   __syncthreads();
   for (int b = blockIdx.x; b < nbricks; b += gridDim.x) {
     const int bb = brick_of(b);
     const int lo = bb * B;
-    const int2 cnt = bk.count[bb];
+    const int4 cnt = bk.info[bb];
     const int bn = b + (int)gridDim.x;
     const int nbb = bn < nbricks ? brick_of(bn) : -1;
     const int ne = (cnt.x + 1) & ~1;  // an even number of entries: 16-byte multiples of the 24-byte centroids
+    // the pool of this brick: halo rows, then {n, area}, then centroids
+    double* s_geo = reinterpret_cast<double*>(brick_smem + L::pool + ((cnt.y * NV * 8 + 31) & ~31));
+    double* s_fcen = s_geo + 4 * ne;
     if (cnt.x >= 0) {
       if (tid == 0) {
         mbar_expect(&bar, (unsigned)(B * NV * 8 + B * 24 + B * 8 + 3072 + ne * 56));
         bulk_copy(s_ri, bk.idx + (size_t)bb * 1536, 3072, &bar);
         bulk_copy(s_row, src + (size_t)lo * NV, B * NV * 8, &bar);
         if (ne) {
-          bulk_copy(s_geo, bk.geo + (size_t)bb * kBrickFcap * 4, (unsigned)ne * 32, &bar);
-          bulk_copy(s_fcen, bk.fcen + (size_t)bb * kBrickFcap * 3, (unsigned)ne * 24, &bar);
+          bulk_copy(s_geo, bk.geo + (size_t)cnt.z * 4, (unsigned)ne * 32, &bar);
+          bulk_copy(s_fcen, bk.fcen + (size_t)cnt.z * 3, (unsigned)ne * 24, &bar);
         }
         bulk_copy(s_cen, m.cen + 3 * (size_t)lo, B * 24, &bar);
         bulk_copy(s_ivol, m.ivol + lo, B * 8, &bar);
@@ -675,17 +681,17 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
       }
     }
     if (nbb >= 0) {  // the next brick: its halo list into the other buffer, its streams towards L2
-      int* hn = s_hl + (buf ^ 1) * kBrickHalo;
-      for (int i = tid; i < kBrickHalo; i += B) hn[i] = bk.halo[(size_t)nbb * kBrickHalo + i];
-      if (tid == 32) {
-        const int2 c2 = bk.count[nbb];
-        if (c2.x >= 0) {
+      const int4 c2 = bk.info[nbb];
+      if (c2.x >= 0) {
+        int* hn = s_hl + (buf ^ 1) * kBrickHalo;
+        for (int i = tid; i < c2.y; i += B) hn[i] = bk.halo[(size_t)c2.w + i];
+        if (tid == 32) {
           const int n2 = (c2.x + 1) & ~1;
           bulk_prefetch_l2(bk.idx + (size_t)nbb * 1536, 3072);
           bulk_prefetch_l2(src + (size_t)nbb * B * NV, B * NV * 8);
           if (n2) {
-            bulk_prefetch_l2(bk.geo + (size_t)nbb * kBrickFcap * 4, (unsigned)n2 * 32);
-            bulk_prefetch_l2(bk.fcen + (size_t)nbb * kBrickFcap * 3, (unsigned)n2 * 24);
+            bulk_prefetch_l2(bk.geo + (size_t)c2.z * 4, (unsigned)n2 * 32);
+            bulk_prefetch_l2(bk.fcen + (size_t)c2.z * 3, (unsigned)n2 * 24);
           }
           bulk_prefetch_l2(m.cen + 3 * (size_t)nbb * B, B * 24);
         }
@@ -790,21 +796,27 @@ __global__ void __launch_bounds__(kBrick, TAFV_K1B_MINB) k_grad_limit_brick(Mesh
   }
 }
 
-// The static brick structures (BrickDev) of cells [0, n), one block per whole
-// brick: a slot whose face this cell owns as the left side (or whose left cell
-// lies outside the brick) takes a packed face entry, the other side of a face
+// The static brick structures (BrickDev) of cells [0, 128 nbricks), one block
+// per brick, in two passes around an exclusive scan of the bricks' sizes: a
+// slot whose face this cell owns as the left side (or whose left cell lies
+// outside the brick) takes a packed face entry, the other side of a face
 // inside the brick shares its left cell's entry; every out-of-brick neighbour
-// takes a halo row. A brick that does not fit the stage gets count.x = -1.
+// takes a halo row. FILL = false: sizes only (info.x < 0: the brick does not
+// fit the stage; esize / hsize = its padded sizes, 0 when ragged); FILL = true:
+// info.z / .w hold the offsets and the tables are written.
+template <bool FILL>
 __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ adj_nb,
                                                         const int* __restrict__ adj_face,
                                                         const double4* __restrict__ geo,
-                                                        const double* __restrict__ fcen, int nbricks,
-                                                        unsigned short* idx, int* halo, double* bgeo, double* bfcen,
-                                                        int2* count, int* ragged_count) {
+                                                        const double* __restrict__ fcen, int nbricks, int nv,
+                                                        int4* info, int* esize, int* hsize, unsigned short* idx,
+                                                        int* halo, double* bgeo, double* bfcen,
+                                                        int* ragged_count) {
   __shared__ int s_nb[768], s_af[768], s_ent[768];
   __shared__ int s_e[kBrick + 1], s_h[kBrick + 1];
   const int b = blockIdx.x, tid = threadIdx.x, lo = b * kBrick;
   if (b >= nbricks) return;
+  if (FILL && info[b].x < 0) return;
   for (int i = tid; i < 768; i += kBrick) {
     s_nb[i] = adj_nb[6 * (size_t)lo + i];
     s_af[i] = adj_face[6 * (size_t)lo + i];
@@ -829,12 +841,17 @@ __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ 
   }
   __syncthreads();
   const int etot = s_e[kBrick], htot = s_h[kBrick];
-  const bool fits = etot <= kBrickFcap && htot <= kBrickHalo;
-  if (tid == 0) {
-    count[b] = fits ? make_int2(etot, htot) : make_int2(-etot, htot);  // x < 0: ragged (sizes kept for tuning)
-    if (!fits) atomicAdd(ragged_count, 1);
+  if (!FILL) {
+    if (tid == 0) {
+      const bool fits = htot <= kBrickHalo && brick_pool_bytes(etot, htot, nv) <= kBrickPool;
+      info[b] = make_int4(fits ? etot : -etot - 1, htot, 0, 0);  // ragged sizes kept for tuning
+      esize[b] = fits ? (etot + 1) & ~1 : 0;
+      hsize[b] = fits ? (htot + 3) & ~3 : 0;
+      if (!fits) atomicAdd(ragged_count, 1);
+    }
+    return;
   }
-  if (!fits) return;
+  const size_t eoff = (size_t)info[b].z, hoff = (size_t)info[b].w;
   int e = s_e[tid], h = s_h[tid];
   unsigned short* ri = idx + (size_t)b * 1536;
   unsigned short* fi = ri + 768;
@@ -846,7 +863,7 @@ __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ 
       if (inside) {
         r = (unsigned short)(nb - lo);
       } else {
-        halo[(size_t)b * kBrickHalo + h] = nb;
+        halo[hoff + h] = nb;
         r = (unsigned short)(kBrick + h);
         ++h;
       }
@@ -856,12 +873,12 @@ __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ 
     if (ef >= 0 || !inside) {
       const int f = ef >= 0 ? ef : ~ef;
       const double4 gq = geo[f];
-      double* go = bgeo + ((size_t)b * kBrickFcap + e) * 4;
+      double* go = bgeo + (eoff + e) * 4;
       go[0] = gq.x;
       go[1] = gq.y;
       go[2] = gq.z;
       go[3] = gq.w;
-      double* fo = bfcen + ((size_t)b * kBrickFcap + e) * 3;
+      double* fo = bfcen + (eoff + e) * 3;
       fo[0] = fcen[3 * (size_t)f];
       fo[1] = fcen[3 * (size_t)f + 1];
       fo[2] = fcen[3 * (size_t)f + 2];
@@ -869,7 +886,6 @@ __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ 
     }
     s_ent[tid * 6 + t] = ent;
   }
-  for (int i = htot + tid; i < kBrickHalo; i += kBrick) halo[(size_t)b * kBrickHalo + i] = 0;  // (never gathered)
   __syncthreads();
   for (int t = 0; t < 6; ++t) {
     const int nb = s_nb[tid * 6 + t], ef = s_af[tid * 6 + t];
@@ -882,11 +898,18 @@ __global__ void __launch_bounds__(kBrick) k_brick_build(const int* __restrict__ 
     fi[tid * 6 + t] = (unsigned short)(ent | (ef < 0 ? 0x8000 : 0));
   }
 }
+// Offsets (exclusive scans of the padded sizes) into info.z / .w.
+__global__ void k_brick_offsets(int4* info, const int* eoff, const int* hoff, int nbricks) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbricks; b += gridDim.x * blockDim.x) {
+    info[b].z = eoff[b];
+    info[b].w = hoff[b];
+  }
+}
 // The cells the brick kernel leaves to k_grad_limit: ragged bricks and the tail.
-__global__ void k_brick_ragged_cells(const int2* __restrict__ count, int nbricks, int n, int* list, int* n_out) {
+__global__ void k_brick_ragged_cells(const int4* __restrict__ info, int nbricks, int n, int* list, int* n_out) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const int b = c / kBrick;
-    if (b >= nbricks || count[b].x < 0) list[atomicAdd(n_out, 1)] = c;
+    if (b >= nbricks || info[b].x < 0) list[atomicAdd(n_out, 1)] = c;
   }
 }
 

@@ -72,7 +72,7 @@ void check_cuda(cudaError_t e, const char* where) {
 }
 #define CK(x) check_cuda((x), #x)
 #ifndef TAFV_K1_BRICK_MAX_RAGGED
-#define TAFV_K1_BRICK_MAX_RAGGED 0.4  // auto mode: largest share of bricks that may not fit the stage
+#define TAFV_K1_BRICK_MAX_RAGGED 0.25  // auto mode: largest share of bricks that may not fit the stage
 #endif
 #ifndef TAFV_K1_BRICK_AUTO
 #define TAFV_K1_BRICK_AUTO (4 << 20)  // auto threshold (owned cells) of the brick K1
@@ -180,11 +180,12 @@ struct tafv_gpu {
   unsigned short* brick_idx = nullptr;
   int* brick_halo = nullptr;
   double *brick_geo = nullptr, *brick_fcen = nullptr;
-  int2* brick_count = nullptr;
+  int4* brick_info = nullptr;
+  long long brick_entries = 0;
   int *brick_rest = nullptr, *brick_nrest = nullptr;  // list and its count (device)
   int brick_rest_host = 0, brick_ragged = 0, nbricks = 0;
   bool brick_declined = false;  // auto mode found too many ragged bricks on this mesh
-  BrickDev brick_dev() const { return BrickDev{brick_idx, brick_halo, brick_geo, brick_fcen, brick_count}; }
+  BrickDev brick_dev() const { return BrickDev{brick_idx, brick_info, brick_halo, brick_geo, brick_fcen}; }
   int grid_k1b = 0;
   bool use_k1_brick() const {
     return deg6 && brick_idx && (k1_brick > 0 || (k1_brick < 0 && n_own >= (TAFV_K1_BRICK_AUTO)));
@@ -368,7 +369,7 @@ struct tafv_gpu {
     if (iter_graph) cudaGraphExecDestroy(iter_graph);
     if (owns_mesh) {
       void* mesh_ptrs[] = {vol, ivol, cen, chl, fcen, sgeo, sdx, fdx, adj_off, adj_face, adj_nb, lr, rcf, geo,
-                           d_cperm, d_fperm, bface, brick_idx, brick_halo, brick_geo, brick_fcen, brick_count,
+                           d_cperm, d_fperm, bface, brick_idx, brick_halo, brick_geo, brick_fcen, brick_info,
                            brick_rest, brick_nrest};
       for (void* p : mesh_ptrs)
         if (p) cudaFree(p);
@@ -1058,44 +1059,70 @@ void build_bricks(tafv_gpu& h) {
   if (h.brick_declined && h.k1_brick < 0) return;
   const int nb = h.N / kBrick;
   h.nbricks = nb;
-  h.brick_idx = dalloc<unsigned short>((size_t)nb * 1536);
-  h.brick_halo = dalloc<int>((size_t)nb * kBrickHalo);
-  h.brick_geo = dalloc<double>((size_t)nb * kBrickFcap * 4);
-  h.brick_fcen = dalloc<double>((size_t)nb * kBrickFcap * 3);
-  h.brick_count = dalloc<int2>(nb);
+  h.brick_info = dalloc<int4>(nb);
   h.brick_nrest = dalloc<int>(2);
+  int* esize = dalloc<int>((size_t)nb + 1);
+  int* hsize = dalloc<int>((size_t)nb + 1);
+  int* eoff = dalloc<int>((size_t)nb + 1);
+  int* hoff = dalloc<int>((size_t)nb + 1);
+  auto drop = [&] {
+    for (void* p : {(void*)esize, (void*)hsize, (void*)eoff, (void*)hoff}) cudaFree(p);
+  };
   CK(cudaMemsetAsync(h.brick_nrest, 0, 2 * sizeof(int), h.st));
-  CK(cudaMemsetAsync(h.brick_halo, 0, (size_t)nb * kBrickHalo * sizeof(int), h.st));
-  CK(cudaMemsetAsync(h.brick_geo, 0, (size_t)nb * kBrickFcap * 4 * sizeof(double), h.st));
-  CK(cudaMemsetAsync(h.brick_fcen, 0, (size_t)nb * kBrickFcap * 3 * sizeof(double), h.st));
-  k_brick_build<<<nb, kBrick, 0, h.st>>>(h.adj_nb, h.adj_face, h.geo, h.fcen, nb, h.brick_idx, h.brick_halo,
-                                         h.brick_geo, h.brick_fcen, h.brick_count, h.brick_nrest + 1);
+  CK(cudaMemsetAsync(esize, 0, ((size_t)nb + 1) * sizeof(int), h.st));
+  CK(cudaMemsetAsync(hsize, 0, ((size_t)nb + 1) * sizeof(int), h.st));
+  k_brick_build<false><<<nb, kBrick, 0, h.st>>>(h.adj_nb, h.adj_face, h.geo, h.fcen, nb, h.nv, h.brick_info, esize,
+                                                hsize, nullptr, nullptr, nullptr, nullptr, h.brick_nrest + 1);
   CK(cudaGetLastError());
-  int cnt[2] = {0, 0};
+  // offsets: exclusive scans over nb + 1 sizes (the last entries are the totals)
+  size_t need = 0, need2 = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, need, esize, eoff, nb + 1, h.st));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, need2, hsize, hoff, nb + 1, h.st));
+  need = std::max(need, need2);
+  void* tmp = nullptr;
+  CK(cudaMalloc(&tmp, std::max<size_t>(need, 16)));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, need, esize, eoff, nb + 1, h.st));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, need, hsize, hoff, nb + 1, h.st));
+  int cnt[2] = {0, 0}, etot = 0, htot = 0;
   CK(cudaMemcpyAsync(cnt, h.brick_nrest, sizeof cnt, cudaMemcpyDeviceToHost, h.st));
+  CK(cudaMemcpyAsync(&etot, eoff + nb, sizeof(int), cudaMemcpyDeviceToHost, h.st));
+  CK(cudaMemcpyAsync(&htot, hoff + nb, sizeof(int), cudaMemcpyDeviceToHost, h.st));
   CK(cudaStreamSynchronize(h.st));
+  cudaFree(tmp);
   h.brick_ragged = cnt[1];
   // auto mode: the brick kernel pays only when most bricks fit its stage
-  // (config 4: 75 % fit, K1 -8 %; config 3's corner-stretched mesh: ~40 %,
-  // K1 +7 % with the rest on the general kernel) -- else drop the structures
+  // (config 4: 92 % fit, K1 -15 %; config 5: all fit; config 3's
+  // corner-stretched mesh: 61 %, K1 +2-7 % with the rest on the general
+  // kernel) -- else drop the structures
   if (h.k1_brick < 0 && (double)cnt[1] > TAFV_K1_BRICK_MAX_RAGGED * nb) {
-    void* ptrs[] = {h.brick_idx, h.brick_halo, h.brick_geo, h.brick_fcen, h.brick_count, h.brick_nrest};
-    for (void* p : ptrs) cudaFree(p);
-    h.brick_idx = nullptr;
-    h.brick_halo = nullptr;
-    h.brick_geo = h.brick_fcen = nullptr;
-    h.brick_count = nullptr;
+    drop();
+    cudaFree(h.brick_info);
+    cudaFree(h.brick_nrest);
+    h.brick_info = nullptr;
     h.brick_nrest = nullptr;
     h.brick_declined = true;
     return;
   }
+  k_brick_offsets<<<h.grid_for(nb, 256), 256, 0, h.st>>>(h.brick_info, eoff, hoff, nb);
+  h.brick_idx = dalloc<unsigned short>((size_t)nb * 1536);
+  h.brick_halo = dalloc<int>(std::max(1, htot));
+  h.brick_geo = dalloc<double>((size_t)std::max(1, etot) * 4);
+  h.brick_fcen = dalloc<double>((size_t)std::max(1, etot) * 3);
+  CK(cudaMemsetAsync(h.brick_halo, 0, (size_t)std::max(1, htot) * sizeof(int), h.st));
+  CK(cudaMemsetAsync(h.brick_geo, 0, (size_t)std::max(1, etot) * 4 * sizeof(double), h.st));
+  CK(cudaMemsetAsync(h.brick_fcen, 0, (size_t)std::max(1, etot) * 3 * sizeof(double), h.st));
+  k_brick_build<true><<<nb, kBrick, 0, h.st>>>(h.adj_nb, h.adj_face, h.geo, h.fcen, nb, h.nv, h.brick_info, esize,
+                                               hsize, h.brick_idx, h.brick_halo, h.brick_geo, h.brick_fcen, nullptr);
+  CK(cudaGetLastError());
   const size_t cap = (size_t)cnt[1] * kBrick + (size_t)(h.N - nb * kBrick);
   h.brick_rest = dalloc<int>(std::max<size_t>(1, cap));
-  k_brick_ragged_cells<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.brick_count, nb, h.N, h.brick_rest, h.brick_nrest);
+  k_brick_ragged_cells<<<h.grid_for(h.N, 256), 256, 0, h.st>>>(h.brick_info, nb, h.N, h.brick_rest, h.brick_nrest);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(cnt, h.brick_nrest, sizeof(int), cudaMemcpyDeviceToHost, h.st));
   CK(cudaStreamSynchronize(h.st));
+  drop();
   h.brick_rest_host = cnt[0];
+  h.brick_entries = etot;
   if ((size_t)cnt[0] != cap) throw std::logic_error("brick K1: ragged cell count mismatch");
 }
 
@@ -2648,7 +2675,7 @@ tafv_gpu* make_twin(const tafv_gpu& h) {
     t->brick_halo = h.brick_halo;
     t->brick_geo = h.brick_geo;
     t->brick_fcen = h.brick_fcen;
-    t->brick_count = h.brick_count;
+    t->brick_info = h.brick_info;
     t->brick_rest = h.brick_rest;
     t->brick_nrest = h.brick_nrest;
     t->brick_rest_host = h.brick_rest_host;
@@ -2994,9 +3021,9 @@ int tafv_gpu_get_array(tafv_gpu* h, const char* name, void* out) {
     if (n == "w") rows(h->w, h->N, h->nv, h->d_cperm);
     else if (n == "W") rows(h->W, h->N, h->nv, h->d_cperm);
     else if (n == "repartition_ms") *static_cast<double*>(out) = h->rep_ms;
-    else if (n == "brick_counts") {  // [nbricks][2] int32: face entries (negative: ragged), halo rows
-      if (h->brick_count)
-        CK(cudaMemcpy(out, h->brick_count, (size_t)h->nbricks * sizeof(int2), cudaMemcpyDeviceToHost));
+    else if (n == "brick_counts") {  // [nbricks][4] int32: face entries (-e - 1: ragged), halo rows, offsets
+      if (h->brick_info)
+        CK(cudaMemcpy(out, h->brick_info, (size_t)h->nbricks * sizeof(int4), cudaMemcpyDeviceToHost));
     } else if (n == "brick_info") {  // bricks, ragged bricks, cells left to the general K1, built
       double* o = static_cast<double*>(out);
       o[0] = h->nbricks;
